@@ -1,0 +1,164 @@
+/*
+ * freqcache_b200.h — C ABI of the B200-native FreqCache token-cache decision
+ * path (select + splice).  Built for sm_100a; device pointers only; every call
+ * is asynchronous on the caller's CUDA stream; no hidden global state (all
+ * per-geometry constants live in an explicit fc_plan, all per-stream state in
+ * caller-owned memory).
+ *
+ * The reference (arxiv 2604.24391 CPU package, /root/reference/pkg) has no
+ * FFI: its operator API is the Python export list
+ * pkg/src/freqcache/__init__.py:11-98.  Each entry point below names the
+ * reference function(s) it replaces:
+ *
+ *   fc_select        fusion.py:121-242  decide()  (+ frame.py:6-15 validate,
+ *                    frameio.py:26,85-88 luma, migration.py:87-185,
+ *                    edge_refresh.py:48-73, budget.py:34-75,
+ *                    fusion.py:104-115 topk_ascending, :245-262 invariants)
+ *                    batched over B independent streams; the previous
+ *                    frame's spectrum is carried in `state`, so each frame is
+ *                    transformed once (the reference transforms both frames
+ *                    of every pair).
+ *   fc_splice        fusion.py:462-512  step()  token gather/scatter + ages
+ *   fc_splice_map    fusion.py:481-504  reuse-source / recompute-order map of
+ *                    an arbitrary (host-built) CacheDecision
+ *   fc_patch_energy  edge_refresh.py:48-59 patch_energy()
+ *   fc_state_reset   fusion.py:450-459 populate_cache() cold start (the next
+ *                    fc_select on a reset stream establishes its spectrum)
+ */
+#ifndef FREQCACHE_B200_H
+#define FREQCACHE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FC_ABI_VERSION 1
+
+/* status codes (fc_strerror) */
+#define FC_OK            0
+#define FC_EINVAL        1  /* bad argument -> ValueError in the facade      */
+#define FC_EUNSUPPORTED  2  /* geometry outside the kernel envelope          */
+#define FC_ECUDA         3  /* CUDA runtime error                            */
+#define FC_ENONFINITE    4  /* per stream: frame has NaN/Inf (frame.py:13)   */
+#define FC_EPSI          5  /* per stream: psi outside [0,1] (budget.py:69)  */
+#define FC_EBOUNDS       6  /* splice source out of bounds (fusion.py:488)   */
+
+/* CacheDecision.diagnostic codes */
+#define FC_DIAG_NONE        0
+#define FC_DIAG_DEGENERATE  1  /* "degenerate spectrum"                     */
+#define FC_DIAG_NO_TEXTURE  2  /* "no texture; displacement undefined"      */
+
+/* frame formats */
+#define FC_FMT_RGB_F32   0  /* [B][H][W][3] float32, BT.601 luma in fp64     */
+#define FC_FMT_GRAY_F32  1  /* [B][H][W]    float32                          */
+#define FC_FMT_GRAY_F64  2  /* [B][H][W]    float64 (the reference's frames) */
+
+/* fresh-row layouts for fc_splice */
+#define FC_FRESH_DENSE    0  /* fresh row of token p is fresh[b][p]          */
+#define FC_FRESH_COMPACT  1  /* k-th recomputed token (row-major) is fresh[b][k] */
+
+typedef struct fc_geometry {
+  int32_t batch;        /* independent streams B                            */
+  int32_t height;       /* H                                                */
+  int32_t width;        /* W                                                */
+  int32_t patch_size;   /* P (CacheConfig.patch_size), divides H and W      */
+  int32_t format;       /* FC_FMT_*                                         */
+} fc_geometry;
+
+/* CacheConfig + BudgetConfig (fusion.py:52-67, budget.py:12-24) */
+typedef struct fc_config {
+  double tau_mig;        /* 0.12 */
+  double edge_lambda;    /* 0.25 */
+  double alpha_min;      /* 0.08 */
+  double alpha_max;      /* 0.5  */
+  int32_t refresh_shift; /* <0: reference behaviour; k>=0: flush when
+                            max(|di_p|,|dj_p|) > k (BASELINE config 2)      */
+  int32_t reserved;
+} fc_config;
+
+/* One stream's CacheDecision scalars (fusion.py:70-94). */
+typedef struct fc_stream_result {
+  int32_t status;       /* FC_OK / FC_ENONFINITE / FC_EPSI                  */
+  int32_t cold;         /* 1: no previous frame — everything recomputed    */
+  int32_t flushed;
+  int32_t diagnostic;   /* FC_DIAG_*                                        */
+  int32_t k_reuse;
+  int32_t k_candidate;
+  int32_t k_final;
+  int32_t n_refresh;
+  int32_t di, dj, di_patches, dj_patches;
+  int32_t rows, cols;
+  int64_t bin_count;
+  double sim_freq;
+  double entropy_raw;
+  double entropy_norm;
+  double alpha;
+  double energy_mean;
+  double energy_std;
+  double energy_threshold;
+  double peak;           /* phase-correlation peak (ifft2 normalisation)   */
+  double peak_runner_up; /* largest other response value                  */
+} fc_stream_result;
+
+/* Device output buffers of fc_select (caller-allocated, N = rows*cols). */
+typedef struct fc_select_out {
+  fc_stream_result* results; /* [B]                                          */
+  int32_t* reuse_idx;        /* [B][N] ascending (E, idx), -1 padded          */
+  int32_t* recompute_idx;    /* [B][N] row-major, -1 padded                   */
+  int32_t* src_map;          /* [B][N] >=0: cache row; <0: -(rank+1) fresh   */
+  uint8_t* reuse_mask;       /* [B][N]                                        */
+  uint8_t* refresh_mask;     /* [B][N]                                        */
+  double*  energy;           /* [B][N] high-pass DCT energy                   */
+} fc_select_out;
+
+typedef struct fc_plan fc_plan;
+
+int  fc_abi_version(void);
+const char* fc_strerror(int code);
+
+/* Plan: validates the geometry, uploads twiddles / DCT basis, sizes the
+ * workspace.  Not thread-safe against concurrent destroy. */
+int  fc_plan_create(const fc_geometry* geom, fc_plan** out);
+void fc_plan_destroy(fc_plan* plan);
+int64_t fc_plan_state_bytes(const fc_plan* plan);     /* per-stream state x B */
+int64_t fc_plan_workspace_bytes(const fc_plan* plan); /* scratch             */
+int  fc_plan_tokens(const fc_plan* plan);             /* N = rows*cols        */
+
+/* Mark streams [first, first+count) cold. */
+int  fc_state_reset(const fc_plan* plan, void* state, int32_t first,
+                    int32_t count, void* cuda_stream);
+
+/* One decision step for all B streams (frames: [B] frames in geometry's
+ * format).  Cold streams only establish their spectrum (result.cold = 1). */
+int  fc_select(const fc_plan* plan, const fc_config* cfg, const void* frames,
+               void* state, void* workspace, const fc_select_out* out,
+               void* cuda_stream);
+
+/* High-pass block-DCT energy of B frames (edge_refresh.py:48-59); energy is
+ * [B][N] float64.  Uses the plan's workspace. */
+int  fc_patch_energy(const fc_plan* plan, const void* frames, void* workspace,
+                     double* energy, void* cuda_stream);
+
+/* Splice: out[b][p] = src_map[b][p] >= 0 ? cache[b][src] : fresh[b][...];
+ * out_ages likewise (cache_ages+1 / 0).  cache may be NULL when every entry
+ * of src_map is negative.  row_bytes = D * element size (any, bit copy). */
+int  fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes,
+               const int32_t* src_map, const void* cache,
+               const int64_t* cache_ages, const void* fresh,
+               int32_t fresh_layout, void* out, int64_t* out_ages,
+               void* cuda_stream);
+
+/* Build src_map for one stream from an ordered reuse list (fusion.py:481-504).
+ * flag (device int32, may be NULL) receives FC_EBOUNDS on an out-of-bounds
+ * source. */
+int  fc_splice_map(int32_t rows, int32_t cols, const int32_t* reuse_idx,
+                   int32_t k, int32_t di_patches, int32_t dj_patches,
+                   int32_t* src_map, int32_t* flag, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FREQCACHE_B200_H */

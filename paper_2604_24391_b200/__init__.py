@@ -1,0 +1,51 @@
+"""B200-native FreqCache token-cache decision path (arXiv 2604.24391).
+
+Drop-in for the reference package's decision path (``freqcache``,
+``pkg/src/freqcache/__init__.py:11-98``): same names, signatures and error
+behaviour for the path's entry points, executed by hand-written sm_100a
+kernels behind the C ABI in ``include/freqcache_b200.h``.  The batched,
+device-resident API for many streams per GPU is :class:`FreqCacheEngine`.
+
+Importing the package does not need a GPU; calling into the path does (no
+CPU fallback).
+"""
+
+__version__ = "0.1.0"
+
+from .types import (  # noqa: F401
+    DEFAULT_COST_MODEL,
+    BudgetConfig,
+    CacheConfig,
+    CacheDecision,
+    ConstantFrameError,
+    CostModel,
+    DegenerateSpectrumError,
+    Displacement,
+    EnergyMap,
+    EntropyReading,
+    FrameParseError,
+    GateAction,
+    RefreshMask,
+    SequenceReport,
+    StepReport,
+    TokenCache,
+)
+from .geometry import PatchGrid, validate_frame  # noqa: F401
+from .stages import (  # noqa: F401
+    CROSS_POWER_EPS,
+    alignment_mask,
+    cutoff_index,
+    highpass_filter,
+    migration_gate,
+    reuse_budget,
+)
+from .api import (  # noqa: F401
+    decide,
+    default_token_fn,
+    patch_energy,
+    phase_correlation,
+    populate_cache,
+    run_sequence,
+    step,
+)
+from .engine import FreqCacheEngine, SelectResult, splice, splice_map  # noqa: F401

@@ -1,0 +1,316 @@
+"""Drop-in entry points with the reference's names and signatures.
+
+``decide`` / ``step`` / ``populate_cache`` / ``run_sequence`` behave like
+the reference's (fusion.py:121-242, 450-572) but execute on the GPU through
+the C ABI: frames are uploaded, the sm_100a kernels compute the spectra,
+masks, budget and top-K, and the token splice runs as a device gather.
+``token_fn`` stays a host callable, exactly as in the reference (it is the
+model that produces fresh token states).  Raises if the CUDA library or a
+device is missing — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .engine import FreqCacheEngine, splice, splice_map
+from .geometry import PatchGrid, coerce_frame, grid_shape
+from .types import (
+    DEFAULT_COST_MODEL,
+    CacheDecision,
+    ConstantFrameError,
+    Displacement,
+    EnergyMap,
+    EntropyReading,
+    SequenceReport,
+    StepReport,
+    TokenCache,
+)
+
+_ENGINES = {}
+
+
+def _engine(h, w, p, fmt="gray64", batch=1):
+    key = (h, w, p, fmt, batch, torch.cuda.current_device())
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = FreqCacheEngine(batch, h, w, p, fmt=fmt)
+        _ENGINES[key] = eng
+    return eng
+
+
+def _device_frame(a):
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    return t.to("cuda", non_blocking=False).unsqueeze(0)
+
+
+def _raise_status(res):
+    st = int(res["status"])
+    if st == nat.FC_ENONFINITE:
+        raise ValueError("frame contains non-finite values")
+    if st == nat.FC_EPSI:
+        raise ValueError(f"normalized entropy must lie in [0, 1], got {float(res['entropy_norm'])}")
+    if st != nat.FC_OK:
+        nat.check(st, "fc_select")
+
+
+def decision_from_device(res, reuse_idx, recompute_idx, refresh_mask, step=0, timings=None):
+    """fc_stream_result + index rows (host numpy) -> CacheDecision."""
+    n = int(res["rows"]) * int(res["cols"])
+    kf = int(res["k_final"])
+    return CacheDecision(
+        step=int(step),
+        flushed=bool(res["flushed"]),
+        sim_freq=float(res["sim_freq"]),
+        displacement=Displacement(int(res["di"]), int(res["dj"]), int(res["di_patches"]),
+                                  int(res["dj_patches"])),
+        entropy=EntropyReading(float(res["entropy_raw"]), float(res["entropy_norm"]),
+                               int(res["bin_count"])),
+        alpha_t=float(res["alpha"]),
+        k_reuse=int(res["k_reuse"]),
+        k_candidate=int(res["k_candidate"]),
+        k_final=kf,
+        reuse_set=tuple(int(v) for v in reuse_idx[:kf]),
+        recompute_set=tuple(int(v) for v in recompute_idx[: n - kf]),
+        rows=int(res["rows"]),
+        cols=int(res["cols"]),
+        refresh_set=tuple(int(v) for v in np.flatnonzero(refresh_mask[:n])),
+        diagnostic=nat.DIAG_TEXT[int(res["diagnostic"])],
+        timings_us=dict(timings or {}),
+    )
+
+
+def _fetch(out, row=0):
+    res = out.host_results()[row]
+    ri = out.reuse_idx[row].cpu().numpy()
+    rc = out.recompute_idx[row].cpu().numpy()
+    rm = out.refresh_mask[row].cpu().numpy()
+    return res, ri, rc, rm
+
+
+def assert_decision(d, n):
+    """In-run invariants of a decision (fusion.py:245-262)."""
+    reuse, rec = set(d.reuse_set), set(d.recompute_set)
+    assert not reuse & rec, "reuse and recompute sets overlap"
+    assert len(reuse) + len(rec) == n, "sets do not partition the patches"
+    assert d.k_final == len(d.reuse_set) == min(d.k_reuse, d.k_candidate), \
+        "reuse count does not match the budget rule"
+    if d.flushed:
+        assert d.k_final == 0, "flushed step must reuse nothing"
+    fresh = set(d.refresh_set)
+    rows, cols = d.rows, d.cols
+    dip, djp = d.displacement.di_patches, d.displacement.dj_patches
+    for p in d.reuse_set:
+        i, j = divmod(p, cols)
+        assert 0 <= i - dip < rows and 0 <= j - djp < cols and p not in fresh, \
+            f"reused patch {p} violates alignment/refresh safety"
+
+
+# ------------------------------------------------------------------ decide --
+
+def decide(prev, curr, cfg, *, step=0, parallel=False):
+    """GPU decide (fusion.py:121-242).  ``parallel`` is accepted for API
+    compatibility; the three analyses always run concurrently on the GPU."""
+    prev = coerce_frame(prev)
+    curr = coerce_frame(curr)
+    if prev.shape != curr.shape:
+        raise ValueError(f"frame shapes differ: {prev.shape} vs {curr.shape}")
+    h, w = curr.shape
+    rows, cols = grid_shape(h, w, cfg.patch_size)
+    eng = _engine(h, w, cfg.patch_size)
+    first = getattr(eng, "_aux_out", None)
+    if first is None:
+        first = eng._aux_out = eng.new_output()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tp, tc = _device_frame(prev), _device_frame(curr)
+    start.record()
+    eng.reset()
+    eng.select(tp, cfg, out=first)
+    out = eng.select(tc, cfg)
+    end.record()
+    res0 = first.host_results()[0]
+    _raise_status(res0)
+    res, ri, rc, rm = _fetch(out)
+    _raise_status(res)
+    d = decision_from_device(res, ri, rc, rm, step=step,
+                             timings={"device": int(start.elapsed_time(end) * 1000)})
+    assert_decision(d, rows * cols)
+    return d
+
+
+# -------------------------------------------------------------------- step --
+
+def default_token_fn(patch):
+    """Reference stand-in model (fusion.py:97-101): 16-bin histogram over
+    [0, 1] plus mean and variance.  Host callable, like any token_fn."""
+    p = np.asarray(patch, dtype=np.float64)
+    counts, _ = np.histogram(np.clip(p, 0.0, 1.0), bins=16, range=(0.0, 1.0))
+    return np.concatenate([counts.astype(np.float64), [p.mean(), p.var()]])
+
+
+def populate_cache(frame, patch_size, token_fn):
+    """Cold start: token_fn on every patch, row-major, ages 0 (fusion.py:450-459)."""
+    grid = PatchGrid(frame, patch_size)
+    vecs = [np.asarray(token_fn(grid.patch(*grid.position(q))), dtype=np.float64).ravel()
+            for q in range(grid.n_patches)]
+    tokens = np.stack(vecs).reshape(grid.rows, grid.cols, -1)
+    return TokenCache(tokens, np.zeros((grid.rows, grid.cols), dtype=np.int64))
+
+
+def _fresh_rows(grid, order, token_fn):
+    vecs = [np.asarray(token_fn(grid.patch(*grid.position(q))), dtype=np.float64).ravel()
+            for q in order]
+    return np.stack(vecs) if vecs else None
+
+
+def step(cache, decision, curr, token_fn, cost_model=None):
+    """Apply a decision: device gather of reused slots from their
+    displacement-mapped source, fresh token_fn rows elsewhere
+    (fusion.py:462-512)."""
+    curr = coerce_frame(curr)
+    cost_model = cost_model or DEFAULT_COST_MODEL
+    rows, cols = decision.rows, decision.cols
+    h, w = curr.shape
+    if h % rows or w % cols or h // rows != w // cols:
+        raise ValueError(f"decision grid {rows}x{cols} does not tile frame {h}x{w}")
+    grid = PatchGrid(curr, h // rows)
+    n = grid.n_patches
+    reuse = () if cache is None or decision.flushed else tuple(decision.reuse_set)
+    reused = set(reuse)
+    order = [q for q in range(n) if q not in reused]
+    fresh = _fresh_rows(grid, order, token_fn)
+    dim = fresh.shape[1] if fresh is not None else cache.tokens.shape[2]
+    dev = torch.device("cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    ridx = torch.tensor(reuse, dtype=torch.int32, device=dev) if reuse else None
+    smap = splice_map(rows, cols, ridx, decision.displacement.di_patches,
+                      decision.displacement.dj_patches, flag=flag).view(1, n)
+    if int(flag.item()) != 0:
+        raise AssertionError("reuse source out of bounds")
+    if reuse:
+        ctok = torch.from_numpy(np.ascontiguousarray(cache.tokens, dtype=np.float64)
+                                .reshape(1, n, -1)).to(dev)
+        cage = torch.from_numpy(np.ascontiguousarray(cache.ages, dtype=np.int64).reshape(1, n)).to(dev)
+    else:
+        ctok = cage = None
+    fr = torch.from_numpy(fresh).to(dev).view(1, -1, dim) if fresh is not None else \
+        torch.zeros((1, 1, dim), dtype=torch.float64, device=dev)
+    out = torch.empty((1, n, dim), dtype=torch.float64, device=dev)
+    ages = torch.empty((1, n), dtype=torch.int64, device=dev)
+    splice(smap, ctok, cage, fr, out, ages, compact=True)
+    tokens = out.cpu().numpy().reshape(rows, cols, dim)
+    new_ages = ages.cpu().numpy().reshape(rows, cols)
+    n_rec = n - len(reused)
+    report = StepReport(step=decision.step, n_reused=len(reused), n_recomputed=n_rec,
+                        latency_model_ms=cost_model.latency_ms(n_rec))
+    return TokenCache(tokens, new_ages), report
+
+
+# ------------------------------------------------------------ run_sequence --
+
+def run_sequence(frames, cfg, token_fn=default_token_fn, cost_model=None, parallel=False):
+    """Sequence driver (fusion.py:534-572).  The previous frame's spectrum and
+    the token cache stay on the device between steps, so each frame is
+    transformed once and tokens never round-trip through the host."""
+    if len(frames) < 2:
+        raise ValueError("need at least 2 frames")
+    frames = [coerce_frame(f) for f in frames]
+    shape = frames[0].shape
+    for t, f in enumerate(frames):
+        if f.shape != shape:
+            raise ValueError(f"frame at step {t}: dimension mismatch {f.shape} vs {shape}")
+    cost_model = cost_model or DEFAULT_COST_MODEL
+    h, w = shape
+    p = cfg.patch_size
+    rows, cols = grid_shape(h, w, p)
+    n = rows * cols
+    eng = FreqCacheEngine(1, h, w, p, fmt="gray64")
+    aux = eng.new_output()
+    cache = populate_cache(frames[0], p, token_fn)
+    dim = cache.tokens.shape[2]
+    dev = eng.device
+    tokens = torch.from_numpy(cache.tokens.reshape(1, n, dim).copy()).to(dev)
+    ages = torch.zeros((1, n), dtype=torch.int64, device=dev)
+    eng.select(_device_frame(frames[0]), cfg, out=aux)
+    _raise_status(aux.host_results()[0])
+    decisions, reports = [], []
+    for t in range(1, len(frames)):
+        out = eng.select(_device_frame(frames[t]), cfg)
+        res, ri, rc, rm = _fetch(out)
+        _raise_status(res)
+        d = decision_from_device(res, ri, rc, rm, step=t)
+        assert_decision(d, n)
+        grid = PatchGrid(frames[t], p)
+        fresh = _fresh_rows(grid, d.recompute_set, token_fn)
+        fr = torch.from_numpy(fresh).to(dev).view(1, -1, dim) if fresh is not None else \
+            torch.zeros((1, 1, dim), dtype=torch.float64, device=dev)
+        new_tokens = torch.empty_like(tokens)
+        new_ages = torch.empty_like(ages)
+        splice(out.src_map, tokens, ages, fr, new_tokens, new_ages, compact=True)
+        tokens, ages = new_tokens, new_ages
+        n_rec = n - d.k_final
+        decisions.append(d)
+        reports.append(StepReport(step=t, n_reused=d.k_final, n_recomputed=n_rec,
+                                  latency_model_ms=cost_model.latency_ms(n_rec)))
+    total_reused = sum(d.k_final for d in decisions)
+    mean_latency = sum(r.latency_model_ms for r in reports) / len(reports)
+    baseline = cost_model.latency_ms(n)
+    return SequenceReport(
+        n_frames=len(frames), n_tokens=n, decisions=decisions, step_reports=reports,
+        mean_reuse_ratio=total_reused / (len(decisions) * n), mean_latency_ms=mean_latency,
+        baseline_latency_ms=baseline, speedup=baseline / mean_latency,
+        flush_count=sum(1 for d in decisions if d.flushed),
+    )
+
+
+# --------------------------------------------------------- stage functions --
+
+def _stage_patch(h, w):
+    """A plan patch size for stage calls that do not fix one: the largest
+    divisor of gcd(H, W) in [2, 32] (only the pixel results are used)."""
+    g = math.gcd(h, w)
+    for p in range(min(32, g), 1, -1):
+        if g % p == 0 and (h // p) * (w // p) <= 4096:
+            return p
+    raise nat.NativeError(f"no supported plan geometry for a {h}x{w} frame")
+
+
+def patch_energy(grid):
+    """High-pass block-DCT energy per patch on the GPU (edge_refresh.py:48-59)."""
+    h, w = grid.frame.shape
+    eng = _engine(h, w, grid.patch_size)
+    e = eng.patch_energy(_device_frame(grid.frame))
+    c = max(1, grid.patch_size // 4)
+    return EnergyMap(e.cpu().numpy().reshape(grid.rows, grid.cols), grid.patch_size, c)
+
+
+def phase_correlation(prev, curr, patch_size=1):
+    """Cyclic displacement of curr w.r.t. prev on the GPU (migration.py:108-125)."""
+    prev = coerce_frame(prev)
+    curr = coerce_frame(curr)
+    if prev.shape != curr.shape:
+        raise ValueError(f"frame shapes differ: {prev.shape} vs {curr.shape}")
+    from .types import CacheConfig, BudgetConfig
+    h, w = curr.shape
+    p = _stage_patch(h, w)
+    eng = _engine(h, w, p)
+    first = getattr(eng, "_aux_out", None)
+    if first is None:
+        first = eng._aux_out = eng.new_output()
+    cfg = CacheConfig(patch_size=p, budget=BudgetConfig(0.5, 0.5))
+    eng.reset()
+    eng.select(_device_frame(prev), cfg, out=first)
+    out = eng.select(_device_frame(curr), cfg)
+    res0 = first.host_results()[0]
+    if int(res0["status"]) == nat.FC_ENONFINITE:
+        raise ValueError("frame contains non-finite values")
+    res = out.host_results()[0]
+    if int(res["status"]) == nat.FC_ENONFINITE:
+        raise ValueError("frame contains non-finite values")
+    if int(res["diagnostic"]) in (nat.FC_DIAG_DEGENERATE, nat.FC_DIAG_NO_TEXTURE):
+        raise ConstantFrameError("no texture; displacement undefined")
+    return Displacement.from_pixels(int(res["di"]), int(res["dj"]), patch_size)

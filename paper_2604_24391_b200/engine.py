@@ -1,0 +1,193 @@
+"""Batched device API over the C ABI: many independent streams per GPU.
+
+``FreqCacheEngine`` owns one ``fc_plan`` (geometry), the per-stream state
+(previous-frame spectrum + flags) and the scratch workspace, all in device
+memory allocated through torch.  ``select`` runs one decision step for every
+stream (reference ``decide``, fusion.py:121-242, batched); ``splice`` applies
+the decisions to the hidden-state cache (reference ``step``,
+fusion.py:462-512).  Everything is stream-ordered on torch's current CUDA
+stream, so whole steps can be captured in a CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+_FORMATS = {
+    "rgb": (nat.FC_FMT_RGB_F32, torch.float32, 3),
+    "gray32": (nat.FC_FMT_GRAY_F32, torch.float32, 1),
+    "gray64": (nat.FC_FMT_GRAY_F64, torch.float64, 1),
+}
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _stream(device=None):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def make_config(cfg, refresh_shift=None):
+    """CacheConfig-like object -> fc_config."""
+    b = getattr(cfg, "budget", None)
+    amin = b.alpha_min if b is not None else getattr(cfg, "alpha_min", 0.08)
+    amax = b.alpha_max if b is not None else getattr(cfg, "alpha_max", 0.5)
+    rs = refresh_shift if refresh_shift is not None else getattr(cfg, "refresh_shift", None)
+    return nat.Config(float(cfg.tau_mig), float(cfg.edge_lambda), float(amin), float(amax),
+                      -1 if rs is None else int(rs), 0)
+
+
+@dataclass
+class SelectResult:
+    """Device outputs of one ``select`` step (N = rows*cols tokens)."""
+
+    results: torch.Tensor        # [B, 136] uint8 (fc_stream_result records)
+    reuse_idx: torch.Tensor      # [B, N] int32, ascending (E, idx), -1 padded
+    recompute_idx: torch.Tensor  # [B, N] int32 row-major, -1 padded
+    src_map: torch.Tensor        # [B, N] int32 splice map
+    reuse_mask: torch.Tensor     # [B, N] uint8
+    refresh_mask: torch.Tensor   # [B, N] uint8
+    energy: torch.Tensor         # [B, N] float64
+
+    def host_results(self):
+        return self.results.cpu().numpy().view(nat.RESULT_DTYPE).reshape(-1)
+
+
+class FreqCacheEngine:
+    """Per-GPU batch of ``batch`` independent streams of (H, W) frames."""
+
+    def __init__(self, batch, height, width, patch_size, fmt="rgb", device=None):
+        if fmt not in _FORMATS:
+            raise ValueError(f"unknown frame format {fmt!r}")
+        self.lib = nat.lib()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.fmt = fmt
+        self.format_code, self.dtype, self.channels = _FORMATS[fmt]
+        self.batch, self.height, self.width, self.patch_size = int(batch), int(height), int(width), int(patch_size)
+        geom = nat.Geometry(self.batch, self.height, self.width, self.patch_size, self.format_code)
+        plan = C.c_void_p()
+        with torch.cuda.device(self.device):
+            rc = self.lib.fc_plan_create(C.byref(geom), C.byref(plan))
+        nat.check(rc, "fc_plan_create")
+        self._plan = plan
+        self.rows = self.height // self.patch_size
+        self.cols = self.width // self.patch_size
+        self.n_tokens = self.lib.fc_plan_tokens(plan)
+        sb = self.lib.fc_plan_state_bytes(plan)
+        wb = self.lib.fc_plan_workspace_bytes(plan)
+        self.state = torch.zeros(sb, dtype=torch.uint8, device=self.device)
+        self.workspace = torch.zeros(wb, dtype=torch.uint8, device=self.device)
+        self.out = self.new_output()
+        self.reset()
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and plan.value:
+            try:
+                self.lib.fc_plan_destroy(plan)
+            except Exception:
+                pass
+            self._plan = None
+
+    # ------------------------------------------------------------------
+    def new_output(self):
+        B, N, dev = self.batch, self.n_tokens, self.device
+        return SelectResult(
+            results=torch.zeros((B, nat.RESULT_DTYPE.itemsize), dtype=torch.uint8, device=dev),
+            reuse_idx=torch.empty((B, N), dtype=torch.int32, device=dev),
+            recompute_idx=torch.empty((B, N), dtype=torch.int32, device=dev),
+            src_map=torch.empty((B, N), dtype=torch.int32, device=dev),
+            reuse_mask=torch.empty((B, N), dtype=torch.uint8, device=dev),
+            refresh_mask=torch.empty((B, N), dtype=torch.uint8, device=dev),
+            energy=torch.empty((B, N), dtype=torch.float64, device=dev),
+        )
+
+    def reset(self, first=0, count=None):
+        """Mark streams cold (populate_cache semantics, fusion.py:450-459)."""
+        count = self.batch - first if count is None else count
+        with torch.cuda.device(self.device):
+            nat.check(self.lib.fc_state_reset(self._plan, _ptr(self.state), int(first), int(count),
+                                              _stream(self.device)), "fc_state_reset")
+
+    def frame_shape(self):
+        if self.channels == 3:
+            return (self.batch, self.height, self.width, 3)
+        return (self.batch, self.height, self.width)
+
+    def _check_frames(self, frames):
+        if not isinstance(frames, torch.Tensor) or frames.device != self.device:
+            raise ValueError("frames must be a tensor on the engine's device")
+        if frames.dtype != self.dtype or tuple(frames.shape) != self.frame_shape():
+            raise ValueError(f"frames must be {self.dtype} of shape {self.frame_shape()}, "
+                             f"got {frames.dtype} {tuple(frames.shape)}")
+        if not frames.is_contiguous():
+            raise ValueError("frames must be contiguous")
+
+    def select(self, frames, cfg, out=None, refresh_shift=None):
+        """One decision step for every stream; returns device outputs."""
+        self._check_frames(frames)
+        out = self.out if out is None else out
+        so = nat.SelectOut(out.results.data_ptr(), out.reuse_idx.data_ptr(), out.recompute_idx.data_ptr(),
+                           out.src_map.data_ptr(), out.reuse_mask.data_ptr(), out.refresh_mask.data_ptr(),
+                           out.energy.data_ptr())
+        conf = make_config(cfg, refresh_shift)
+        with torch.cuda.device(self.device):
+            rc = self.lib.fc_select(self._plan, C.byref(conf), _ptr(frames), _ptr(self.state),
+                                    _ptr(self.workspace), C.byref(so), _stream(self.device))
+        nat.check(rc, "fc_select")
+        return out
+
+    def patch_energy(self, frames, energy=None):
+        self._check_frames(frames)
+        if energy is None:
+            energy = torch.empty((self.batch, self.n_tokens), dtype=torch.float64, device=self.device)
+        with torch.cuda.device(self.device):
+            rc = self.lib.fc_patch_energy(self._plan, _ptr(frames), _ptr(self.workspace), _ptr(energy),
+                                          _stream(self.device))
+        nat.check(rc, "fc_patch_energy")
+        return energy
+
+
+def splice(src_map, cache, cache_ages, fresh, out, out_ages, compact=False):
+    """Token splice on device (fusion.py:462-512), any element type.
+
+    src_map [B, N] int32; cache/fresh/out [B, N, D] (fresh may be [B, K, D]
+    front-packed when ``compact``); ages int64 [B, N].  ``cache`` may be None
+    when no entry of src_map is >= 0 (cold start / flush).
+    """
+    lib = nat.lib()
+    B, N = src_map.shape
+    row_bytes = out.shape[-1] * out.element_size()
+    for t in (src_map, fresh, out, out_ages) + ((cache, cache_ages) if cache is not None else ()):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("splice operands must be contiguous CUDA tensors")
+    if cache is not None and (cache.dtype != out.dtype or cache.shape != out.shape):
+        raise ValueError("cache and out must share dtype and shape")
+    if fresh.dtype != out.dtype or fresh.shape[-1] != out.shape[-1]:
+        raise ValueError("fresh rows must match out's dtype and row width")
+    rc = lib.fc_splice(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(cache),
+                       _ptr(cache_ages), _ptr(fresh),
+                       nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE,
+                       _ptr(out), _ptr(out_ages), _stream(out.device))
+    nat.check(rc, "fc_splice")
+    return out, out_ages
+
+
+def splice_map(rows, cols, reuse_idx, di_patches, dj_patches, src_map=None, flag=None):
+    """Device src_map for one stream from an ordered reuse list."""
+    lib = nat.lib()
+    dev = reuse_idx.device if reuse_idx is not None and reuse_idx.numel() else torch.device("cuda")
+    if src_map is None:
+        src_map = torch.empty(rows * cols, dtype=torch.int32, device=dev)
+    k = 0 if reuse_idx is None else int(reuse_idx.numel())
+    rc = lib.fc_splice_map(int(rows), int(cols), _ptr(reuse_idx if k else None), k, int(di_patches),
+                           int(dj_patches), _ptr(src_map), _ptr(flag), _stream(dev))
+    nat.check(rc, "fc_splice_map")
+    return src_map
