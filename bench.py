@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""FreqCache select + splice throughput on B200 (BASELINE config 5 per GPU).
+
+One step = one decision (fc_select: luma + block-DCT energy, 2-D FFT, phase
+correlation, entropy budget, top-K) plus the bf16 hidden-state splice
+(fc_splice, 1024 x 1152 per stream) for every stream on this rank.
+
+Workload per rank (weak scaling, streams sharded with no data-path
+collective): 512 independent streams of 448x448x3 fp32 frames, P=14 (1024
+tokens), adaptive budget, config-2 refresh rule (flush when the patch shift
+exceeds 1), cache/fresh hidden states N(0,1) bf16.  Frames are synthetic
+(paper_2604_24391_b200.synth, torch draw on the GPU, untimed) in a ring of
+24 resident steps (29.6 GB); each step reads 1.23 GB of frames (> L2).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FreqCache select+splice frames/s & tokens/s at 1/2/4/8 B200; % of HBM/TC roofline"
+UNIT = "frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=128)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=512, help="streams per rank")
+    ap.add_argument("--size", type=int, default=448)
+    ap.add_argument("--patch", type=int, default=14)
+    ap.add_argument("--dim", type=int, default=1152)
+    ap.add_argument("--ring", type=int, default=24, help="resident frame steps")
+    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--cpu-streams", type=int, default=64)
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--refresh-shift", type=int, default=1)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------- CPU legs ----
+
+def _cpu_worker(args):
+    """Oracle port on one core: decide + splice for its streams (timed per step)."""
+    streams, steps, warmup, size, patch, dim, refresh_shift, seed = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import numpy as np
+    from oracle import freqcache_oracle as O
+    from paper_2604_24391_b200.synth import stream_frames
+    n = (size // patch) ** 2
+    cfg = O.OracleConfig(patch_size=patch, refresh_shift=refresh_shift)
+    total = warmup + steps + 1
+    data = []
+    for s in streams:
+        fr = stream_frames(seed, s, total, size, size)
+        rng = np.random.default_rng([3000, s])
+        # bf16 hidden states ~ N(0,1), kept as their 16-bit patterns (bit copy)
+        cache = (rng.standard_normal((n, dim), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        fresh = (rng.standard_normal((n, dim), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        data.append((fr, cache, fresh, np.zeros(n, dtype=np.int64)))
+    t_timed = 0.0
+    frames_done = 0
+    for t in range(1, total):
+        t0 = time.perf_counter()
+        for k, (fr, cache, fresh, ages) in enumerate(data):
+            d = O.decide(fr[t - 1], fr[t], cfg, step=t)
+            rec = list(d.recompute_set)
+            cache2, ages2 = O.splice(cache, ages, d, fresh[rec])
+            data[k] = (fr, cache2, fresh, ages2)
+        dt = time.perf_counter() - t0
+        if t > warmup:
+            t_timed += dt
+            frames_done += len(data)
+    return frames_done, t_timed
+
+
+def cpu_run(n_streams, steps, warmup, size, patch, dim, refresh_shift, seed=5000):
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    workers = min(cores, n_streams)
+    parts = [list(range(i, n_streams, workers)) for i in range(workers)]
+    ctx = mp.get_context("spawn")
+    env_keep = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in env_keep:
+        os.environ[k] = "1"
+    try:
+        with ctx.Pool(workers) as pool:
+            res = pool.map(_cpu_worker, [(p, steps, warmup, size, patch, dim, refresh_shift, seed) for p in parts])
+    finally:
+        for k, v in env_keep.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    frames = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return frames / wall if wall > 0 else 0.0, workers, frames
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle port of the reference path on all host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    t0 = time.time()
+    v, cores, frames = cpu_run(a.cpu_streams, a.steps, a.warmup, a.size, a.patch, a.dim, a.refresh_shift)
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * a.cpu_streams / v if v else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (numpy draw of the frozen generator)",
+        "config": {"workload": "config5 sample: decide+splice per frame, 448x448x3 fp32, P=14, N=1024, D=1152",
+                   "streams": a.cpu_streams, "size": a.size, "patch": a.patch, "dim": a.dim,
+                   "refresh_shift": a.refresh_shift},
+        "tokens_per_s": v * (a.size // a.patch) ** 2,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{a.cpu_streams} streams x {a.steps} steps (+{a.warmup} warm-up) of "
+                                   "oracle decide + splice, one process per core, BLAS threads 1"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.time() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU side ----
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2604_24391_b200 import CacheConfig, FreqCacheEngine, splice
+    from paper_2604_24391_b200.synth import torch_stream_frames
+
+    S, H, P, D, R = a.streams, a.size, a.patch, a.dim, a.ring
+    N = (H // P) ** 2
+    cfg = CacheConfig(patch_size=P)
+
+    # ---- inputs, resident in HBM before timing (untimed generation)
+    frames = torch.empty((R, S, H, H, 3), dtype=torch.float32, device=dev)
+    chunk = 64
+    for c0 in range(0, S, chunk):
+        c1 = min(S, c0 + chunk)
+        frames[:, c0:c1] = torch_stream_frames(c1 - c0, R, H, H, seed=5000 + 1000 * rank + c0, device=dev)
+    g = torch.Generator(device=dev).manual_seed(3000 + rank)
+    cache = torch.empty((2, S, N, D), dtype=torch.bfloat16, device=dev)
+    cache[0].normal_(generator=g)
+    fresh = torch.empty((S, N, D), dtype=torch.bfloat16, device=dev).normal_(generator=g)
+    ages = torch.zeros((2, S, N), dtype=torch.int64, device=dev)
+    eng = FreqCacheEngine(S, H, H, P, fmt="rgb", device=dev)
+    torch.cuda.synchronize()
+
+    cur = [0]
+    launches = [0]
+
+    def one_step(t, stage_events=None):
+        fr = frames[t % R]
+        if stage_events is None:
+            out = eng.select(fr, cfg, refresh_shift=a.refresh_shift)
+            launches[0] += 4
+        else:
+            for st in range(4):
+                out = eng.select(fr, cfg, refresh_shift=a.refresh_shift, stage=st)
+                stage_events[st + 1].record()
+            launches[0] += 4
+        i, o = cur[0], 1 - cur[0]
+        splice(out.src_map, cache[i], ages[i], fresh, cache[o], ages[o])
+        launches[0] += 1
+        cur[0] = o
+        return out
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up (step 0 establishes every stream's spectrum)
+    for t in range(a.warmup):
+        one_step(t)
+    barrier()
+
+    # ---- timed region: K steps, CUDA events on the launching stream
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches[0] = 0
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0.record(stream)
+        for t in range(a.warmup, a.warmup + a.steps):
+            one_step(t)
+        ev1.record(stream)
+        barrier()
+    gpu_launches = launches[0]
+    ms = ev0.elapsed_time(ev1)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+    frames_total = S * a.steps * world
+    value = frames_total / (ms / 1e3)
+
+    # decision statistics of the last timed step (sanity, reported)
+    res = eng.out.host_results()
+    reuse_ratio = float(res["k_final"].mean()) / N
+    flush_rate = float(res["flushed"].mean())
+
+    # ---- per-kernel timing pass (same steps, events between launches)
+    kp_steps = min(a.steps, 16)
+    names = ["rows_fwd", "cols", "rows_inv", "select", "splice"]
+    kms = [0.0] * 5
+    t0 = a.warmup + a.steps
+    for t in range(t0, t0 + kp_steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        evs[0].record(stream)
+        one_step(t, stage_events=evs)
+        evs[5].record(stream)
+        torch.cuda.synchronize()
+        for k in range(5):
+            kms[k] += evs[k].elapsed_time(evs[k + 1])
+    kms = [v / kp_steps for v in kms]
+    hw = H * H
+    wcp = ((H // 2 + 7) // 8) * 8
+    spec = 8 * H * wcp
+    kbytes = [
+        S * (12 * hw + spec + 8 * N),          # rows_fwd: RGB in, packed rows out, energies
+        S * (4 * spec),                        # cols: T in/out, state in/out
+        S * spec,                              # rows_inv: T in
+        S * (8 * N + 14 * N + 136),            # select: energies in, masks/indices out
+        S * (4 * N * D + 20 * N),              # splice: one bf16 row in + out per token, map, ages
+    ]
+    dom = max(range(5), key=lambda k: kms[k])
+    hbm, peak_kind = peaks()
+    ach = kbytes[dom] / (kms[dom] / 1e3) / 1e9
+    b_sel = 20 * hw + 16 * N
+    b_spl = 4 * N * D + 20 * N
+    step_ach = (b_sel + b_spl) * (S * a.steps) / (ms / 1e3) / 1e9 if world == 1 else \
+        (b_sel + b_spl) * value / world / 1e9
+    roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "kernel": names[dom], "peak_kind": peak_kind,
+                "bytes_per_launch": kbytes[dom], "ms_per_launch": kms[dom]}
+    roofline_step = {"bound": "hbm", "achieved": step_ach, "peak": hbm, "unit": "GB/s", "frac": step_ach / hbm,
+                     "bytes_per_frame": b_sel + b_spl, "select_bytes": b_sel, "splice_bytes": b_spl}
+    kernels = {names[k]: {"ms": kms[k], "share": kms[k] / sum(kms), "bytes": kbytes[k],
+                          "gbs": kbytes[k] / (kms[k] / 1e3) / 1e9} for k in range(5)}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f)
+        roofline["traffic"] = tr.get(names[dom])
+    except (OSError, ValueError):
+        pass
+
+    # ---- end to end: pinned host frames -> device -> select + splice -> results to host
+    HR = min(4, R)
+    host = torch.empty((HR, S, H, H, 3), dtype=torch.float32, pin_memory=True)
+    for i in range(HR):
+        host[i].copy_(frames[(t0 + kp_steps + i) % R])
+    stage = torch.empty((S, H, H, 3), dtype=torch.float32, device=dev)
+    res_host = torch.empty((S, 136), dtype=torch.uint8, pin_memory=True)
+    map_host = torch.empty((S, N), dtype=torch.int32, pin_memory=True)
+    eng.reset()
+    torch.cuda.synchronize()
+    ke = max(1, a.e2e_steps)
+
+    def e2e_step(i):
+        stage.copy_(host[i % HR], non_blocking=True)
+        out = eng.select(stage, cfg, refresh_shift=a.refresh_shift)
+        j, o = cur[0], 1 - cur[0]
+        splice(out.src_map, cache[j], ages[j], fresh, cache[o], ages[o])
+        cur[0] = o
+        res_host.copy_(out.results, non_blocking=True)
+        map_host.copy_(out.src_map, non_blocking=True)
+
+    e2e_step(0)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(1, ke + 1):
+        e2e_step(i)
+    e1.record(stream)
+    barrier()
+    ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+    e2e_val = S * ke * world / (float(ems.item()) / 1e3)
+    h2d = S * H * H * 3 * 4
+    d2h = S * 136 + S * N * 4
+
+    # ---- CPU baseline (rank 0, N == 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        v, cores, nfr = cpu_run(a.cpu_streams, a.cpu_steps, 1, H, P, D, a.refresh_shift)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{a.cpu_streams} streams x {a.cpu_steps} timed steps of the oracle port "
+                         f"(decide + splice, {nfr} frames), numpy draw of the same generator, "
+                         "one process per core, BLAS threads 1"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (frozen generator, torch draw on GPU; cache/fresh bf16 N(0,1))",
+            "config": {"workload": "config5 per GPU: select + splice, adaptive budget, refresh on shift>1",
+                       "streams_per_gpu": S, "size": H, "channels": 3, "patch": P, "tokens": N,
+                       "hidden": D, "hidden_dtype": "bf16", "frame_ring_steps": R,
+                       "l2": "inputs > L2 (1.23 GB of frames per step, 29.6 GB ring)"},
+            "tokens_per_s": value * N,
+            "roofline": roofline, "roofline_step": roofline_step, "kernels": kernels,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": ke, "path": "pinned host frames -> fc_select -> fc_splice -> results to host"},
+            "gpu_launches": gpu_launches,
+            "clocks": clocks.summary(),
+            "decisions": {"reuse_ratio_last_step": reuse_ratio, "flush_rate_last_step": flush_rate},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

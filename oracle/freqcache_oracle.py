@@ -342,7 +342,8 @@ def splice(cache_tokens, cache_ages, decision, fresh_rows):
     """
     rows, cols = decision.rows, decision.cols
     n = rows * cols
-    dip, djp = decision.displacement[2], decision.displacement[3]
+    disp = decision.displacement
+    dip, djp = (disp.di_patches, disp.dj_patches) if hasattr(disp, "di_patches") else (disp[2], disp[3])
     reuse = () if cache_tokens is None or decision.flushed else decision.reuse_set
     out = np.empty((n,) + np.asarray(fresh_rows).shape[1:], dtype=np.asarray(fresh_rows).dtype)
     ages = np.zeros(n, dtype=np.int64)

@@ -35,6 +35,7 @@ _ENGINES = {}
 
 
 def _engine(h, w, p, fmt="gray64", batch=1):
+    nat.lib()  # raises when the library or a CUDA device is missing
     key = (h, w, p, fmt, batch, torch.cuda.current_device())
     eng = _ENGINES.get(key)
     if eng is None:

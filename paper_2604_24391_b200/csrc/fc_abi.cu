@@ -232,9 +232,10 @@ int fc_state_reset(const fc_plan* pl, void* state, int32_t first, int32_t count,
   return launch_check();
 }
 
-int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
-              const fc_select_out* out, void* stream) {
+int fc_select_stage(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
+                    const fc_select_out* out, int32_t stage, void* stream) {
   if (!pl || !cfg || !frames || !state || !ws || !out) return FC_EINVAL;
+  if (stage < -1 || stage > 3) return FC_EINVAL;
   // CacheConfig / BudgetConfig validation (fusion.py:61-67, budget.py:19-24)
   if (!(cfg->tau_mig >= 0.0 && cfg->tau_mig <= 1.0)) return FC_EINVAL;
   if (!std::isfinite(cfg->edge_lambda)) return FC_EINVAL;
@@ -243,23 +244,28 @@ int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void*
   const KParams kp = bind(pl, state, ws, out->energy);
   const int B = pl->g.batch;
   const dim3 blk(FC_THREADS);
-  {
+  if (stage < 0 || stage == 0) {
     const dim3 grid(kp.rows, B);
     auto fn = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
     fn<<<grid, blk, pl->smemA, st>>>(kp, frames, 1);
   }
-  {
+  if (stage < 0 || stage == 1) {
     const dim3 grid(kp.NCB, B);
     auto fn = (void (*)(KParams))sel_cols(pl->kh);
     fn<<<grid, blk, pl->smemB, st>>>(kp);
   }
-  {
+  if (stage < 0 || stage == 2) {
     const dim3 grid(kp.NRG, B);
     auto fn = (void (*)(KParams))sel_rows_inv(pl->kw);
     fn<<<grid, blk, pl->smemC, st>>>(kp);
   }
-  k_select<<<B, FC_SEL_THREADS, pl->smemD, st>>>(kp, *cfg, *out);
+  if (stage < 0 || stage == 3) k_select<<<B, FC_SEL_THREADS, pl->smemD, st>>>(kp, *cfg, *out);
   return launch_check();
+}
+
+int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
+              const fc_select_out* out, void* stream) {
+  return fc_select_stage(pl, cfg, frames, state, ws, out, -1, stream);
 }
 
 int fc_patch_energy(const fc_plan* pl, const void* frames, void* ws, double* energy, void* stream) {

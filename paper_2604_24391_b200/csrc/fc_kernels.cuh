@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config
   __shared__ double red[32 * 2];
   __shared__ int redi[32];
   __shared__ fc_stream_result R;
-  __shared__ int sh_flush, sh_dip, sh_djp, sh_kfinal, sh_cold, sh_err;
+  __shared__ int sh_flush, sh_dip, sh_djp, sh_kfinal, sh_err;
 
   const double* energy = kp.energy + (size_t)b * N;
   for (int p = threadIdx.x; p < N; p += blockDim.x) E[p] = energy[p];
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config
       else flush = 0;
     }
     R.flushed = flush;
-    sh_flush = flush; sh_dip = dip; sh_djp = djp; sh_cold = cold;
+    sh_flush = flush; sh_dip = dip; sh_djp = djp;
     sh_err = R.status != FC_OK;
     // state for the next step: this frame becomes "prev"
     if (!bad) {

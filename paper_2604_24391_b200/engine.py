@@ -130,8 +130,9 @@ class FreqCacheEngine:
         if not frames.is_contiguous():
             raise ValueError("frames must be contiguous")
 
-    def select(self, frames, cfg, out=None, refresh_shift=None):
-        """One decision step for every stream; returns device outputs."""
+    def select(self, frames, cfg, out=None, refresh_shift=None, stage=-1):
+        """One decision step for every stream; returns device outputs.
+        ``stage`` 0..3 launches a single kernel of the step (timing only)."""
         self._check_frames(frames)
         out = self.out if out is None else out
         so = nat.SelectOut(out.results.data_ptr(), out.reuse_idx.data_ptr(), out.recompute_idx.data_ptr(),
@@ -139,8 +140,9 @@ class FreqCacheEngine:
                            out.energy.data_ptr())
         conf = make_config(cfg, refresh_shift)
         with torch.cuda.device(self.device):
-            rc = self.lib.fc_select(self._plan, C.byref(conf), _ptr(frames), _ptr(self.state),
-                                    _ptr(self.workspace), C.byref(so), _stream(self.device))
+            rc = self.lib.fc_select_stage(self._plan, C.byref(conf), _ptr(frames), _ptr(self.state),
+                                          _ptr(self.workspace), C.byref(so), int(stage),
+                                          _stream(self.device))
         nat.check(rc, "fc_select")
         return out
 
