@@ -242,18 +242,25 @@ def run_ours(a):
     cur = [0]
     launches = [0]
 
-    def one_step(t, stage_events=None):
+    def one_step(t, kernel_ms=None):
         fr = frames[t % R]
-        if stage_events is None:
+        if kernel_ms is None:
             out = eng.select(fr, cfg, refresh_shift=a.refresh_shift)
-            launches[0] += 4
         else:
-            for st in range(4):
-                out = eng.select(fr, cfg, refresh_shift=a.refresh_shift, stage=st)
-                stage_events[st + 1].record()
-            launches[0] += 4
+            prof = []
+            out = eng.select(fr, cfg, refresh_shift=a.refresh_shift, profile=prof)
+            for k in range(4):
+                kernel_ms[k] += prof[k]
+        launches[0] += eng.launches_per_select
         i, o = cur[0], 1 - cur[0]
+        if kernel_ms is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         splice(out.src_map, cache[i], ages[i], fresh, cache[o], ages[o])
+        if kernel_ms is not None:
+            e1.record()
+            torch.cuda.synchronize()
+            kernel_ms[4] += e0.elapsed_time(e1)
         launches[0] += 1
         cur[0] = o
         return out
@@ -299,21 +306,14 @@ def run_ours(a):
     kms = [0.0] * 5
     t0 = a.warmup + a.steps
     for t in range(t0, t0 + kp_steps):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-        evs[0].record(stream)
-        one_step(t, stage_events=evs)
-        evs[5].record(stream)
-        torch.cuda.synchronize()
-        for k in range(5):
-            kms[k] += evs[k].elapsed_time(evs[k + 1])
+        one_step(t, kernel_ms=kms)
     kms = [v / kp_steps for v in kms]
     hw = H * H
-    wcp = ((H // 2 + 7) // 8) * 8
-    spec = 8 * H * wcp
+    spec = 8 * H * ((H // 2 + 7) // 8) * 8   # one packed half-spectrum, fp32 complex
     kbytes = [
-        S * (12 * hw + spec + 8 * N),          # rows_fwd: RGB in, packed rows out, energies
-        S * (4 * spec),                        # cols: T in/out, state in/out
-        S * spec,                              # rows_inv: T in
+        S * (12 * hw + spec + 8 * N),          # rows_fwd: RGB in, packed rows (T1) out, energies
+        S * (4 * spec),                        # cols: T1 in, state in/out, T2 out
+        S * spec,                              # rows_inv: T2 in
         S * (8 * N + 14 * N + 136),            # select: energies in, masks/indices out
         S * (4 * N * D + 20 * N),              # splice: one bf16 row in + out per token, map, ages
     ]

@@ -137,11 +137,12 @@ int  fc_select(const fc_plan* plan, const fc_config* cfg, const void* frames,
                void* state, void* workspace, const fc_select_out* out,
                void* cuda_stream);
 
-/* One stage of fc_select (0: rows_fwd, 1: cols, 2: rows_inv, 3: select) —
- * for per-kernel timing; stages must run in order 0..3 for one step. */
-int  fc_select_stage(const fc_plan* plan, const fc_config* cfg, const void* frames,
-                     void* state, void* workspace, const fc_select_out* out,
-                     int32_t stage, void* cuda_stream);
+/* fc_select with a CUDA event after every launch; synchronises the stream
+ * and returns per-kernel-kind device time in kernel_ms[4] (rows_fwd, cols,
+ * rows_inv, select), summed over stream chunks.  For benchmarking. */
+int  fc_select_profile(const fc_plan* plan, const fc_config* cfg, const void* frames,
+                       void* state, void* workspace, const fc_select_out* out,
+                       float* kernel_ms, void* cuda_stream);
 
 /* High-pass block-DCT energy of B frames (edge_refresh.py:48-59); energy is
  * [B][N] float64.  Uses the plan's workspace. */

@@ -40,7 +40,7 @@ FC_FRESH_COMPACT = 1
 EXPORTS = (
     "fc_abi_version", "fc_strerror", "fc_plan_create", "fc_plan_destroy",
     "fc_plan_state_bytes", "fc_plan_workspace_bytes", "fc_plan_tokens",
-    "fc_state_reset", "fc_select", "fc_select_stage", "fc_patch_energy", "fc_splice",
+    "fc_state_reset", "fc_select", "fc_select_profile", "fc_patch_energy", "fc_splice",
     "fc_splice_map",
 )
 
@@ -105,7 +105,8 @@ def load(path=None):
         "fc_plan_tokens": (C.c_int, [vp]),
         "fc_state_reset": (C.c_int, [vp, vp, i32, i32, vp]),
         "fc_select": (C.c_int, [vp, C.POINTER(Config), vp, vp, vp, C.POINTER(SelectOut), vp]),
-        "fc_select_stage": (C.c_int, [vp, C.POINTER(Config), vp, vp, vp, C.POINTER(SelectOut), i32, vp]),
+        "fc_select_profile": (C.c_int, [vp, C.POINTER(Config), vp, vp, vp, C.POINTER(SelectOut),
+                                        C.POINTER(C.c_float), vp]),
         "fc_patch_energy": (C.c_int, [vp, vp, vp, vp, vp]),
         "fc_splice": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, i32, vp, vp, vp]),
         "fc_splice_map": (C.c_int, [i32, i32, vp, i32, i32, i32, vp, vp, vp]),

@@ -1,6 +1,14 @@
 // C ABI of the B200 FreqCache decision path (see include/freqcache_b200.h).
 // Host side: geometry validation, plan construction (FFT factorisations,
 // fp64-derived twiddles, DCT basis), workspace carving and kernel launches.
+//
+// Two kernel sets implement fc_select:
+//   fast    H = W = 448, P = 14 (BASELINE configs 2-5): register-resident
+//           448-point FFTs (fc_fast448.cuh), streams processed in chunks of
+//           kChunk so the two spectrum intermediates (T1, T2: 0.8 MB per
+//           stream each) stay L2-resident between the three FFT kernels;
+//   generic any other geometry inside the envelope: shared-memory Stockham
+//           FFTs with runtime radix plans (fc_fft.cuh / fc_kernels.cuh).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -10,17 +18,41 @@
 #include <vector>
 
 #include "fc_kernels.cuh"
+#include "fc_fast448.cuh"
+
+namespace {
+constexpr int kChunkDefault = 32;  // streams per A/B/C launch group on the fast path
+constexpr int kLanesDefault = 2;   // concurrent chunk lanes (internal CUDA streams)
+constexpr int kMaxLanes = 8;
+
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* v = std::getenv(name);
+  if (!v) return dflt;
+  const int x = std::atoi(v);
+  return x < lo ? lo : (x > hi ? hi : x);
+}
+}
 
 struct fc_plan {
   fc_geometry g;
   KParams kp;  // geometry + device constant tables (per-call pointers filled at launch)
+  Dct14 dct14;
+  bool fast = false;
+  int chunk = 0;
+  int lanes = 1;                       // fast path: chunk groups in flight
+  cudaStream_t lane[kMaxLanes] = {};   // internal non-blocking streams
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t join[kMaxLanes] = {};
+  size_t lane_stride = 0;              // workspace bytes per lane (T1 + T2)
   float2* d_twW = nullptr;
   float2* d_twH = nullptr;
   double* d_dct = nullptr;
+  float2* d_tw448 = nullptr;
+  float2* d_tw64 = nullptr;
   size_t smemA = 0, smemB = 0, smemC = 0, smemD = 0;
-  size_t off_T = 0, off_stripes = 0, off_stats = 0, off_peaks = 0, off_energy = 0, ws_bytes = 0;
+  size_t off_T = 0, off_T2 = 0, off_stripes = 0, off_stats = 0, off_peaks = 0, off_energy = 0, ws_bytes = 0;
   size_t state_hdr_bytes = 0, state_bytes = 0;
-  int kw = 0, kh = 0;  // fixed-size FFT variants (0 = generic)
+  int kw = 0, kh = 0;  // fixed-size generic FFT variants (0 = runtime plan)
 };
 
 namespace {
@@ -50,16 +82,17 @@ bool factor(int n, FftPlan& pl) {
   return m == 1;
 }
 
+float2 root(long long m, long long n) {
+  const double a = -2.0 * M_PI * (double)(m % n) / (double)n;
+  return make_float2((float)std::cos(a), (float)std::sin(a));
+}
+
 std::vector<float2> twiddles(int n) {
   std::vector<float2> t(n);
-  for (int m = 0; m < n; ++m) {
-    const double a = -2.0 * M_PI * (double)m / (double)n;
-    t[m] = make_float2((float)std::cos(a), (float)std::sin(a));
-  }
+  for (int m = 0; m < n; ++m) t[m] = root(m, n);
   return t;
 }
 
-// kernel pointers selected per fixed-size variant
 template <int N> void* ptr_rows_fwd() { return (void*)k_rows_fwd<N>; }
 template <int N> void* ptr_cols() { return (void*)k_cols<N>; }
 template <int N> void* ptr_rows_inv() { return (void*)k_rows_inv<N>; }
@@ -67,6 +100,12 @@ template <int N> void* ptr_rows_inv() { return (void*)k_rows_inv<N>; }
 void* sel_rows_fwd(int k) { return k == 448 ? ptr_rows_fwd<448>() : k == 224 ? ptr_rows_fwd<224>() : ptr_rows_fwd<0>(); }
 void* sel_cols(int k) { return k == 448 ? ptr_cols<448>() : k == 224 ? ptr_cols<224>() : ptr_cols<0>(); }
 void* sel_rows_inv(int k) { return k == 448 ? ptr_rows_inv<448>() : k == 224 ? ptr_rows_inv<224>() : ptr_rows_inv<0>(); }
+
+void* sel_fast_rows_fwd(int fmt) {
+  return fmt == FC_FMT_RGB_F32 ? (void*)k448_rows_fwd<FC_FMT_RGB_F32>
+       : fmt == FC_FMT_GRAY_F32 ? (void*)k448_rows_fwd<FC_FMT_GRAY_F32>
+                                : (void*)k448_rows_fwd<FC_FMT_GRAY_F64>;
+}
 
 int set_smem(void* fn, size_t bytes) {
   if (bytes > 48 * 1024) {
@@ -87,6 +126,7 @@ KParams bind(const fc_plan* pl, void* state, void* ws, double* energy) {
   KParams kp = pl->kp;
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
   kp.T = reinterpret_cast<float2*>(w + pl->off_T);
+  kp.T2 = pl->fast ? reinterpret_cast<float2*>(w + pl->off_T2) : nullptr;
   kp.stripes = reinterpret_cast<StripeStat*>(w + pl->off_stripes);
   kp.stats = reinterpret_cast<double*>(w + pl->off_stats);
   kp.peaks = reinterpret_cast<PeakPart*>(w + pl->off_peaks);
@@ -100,6 +140,80 @@ KParams bind(const fc_plan* pl, void* state, void* ws, double* energy) {
     kp.spec = nullptr;
   }
   return kp;
+}
+
+int check_cfg(const fc_config* cfg) {
+  // CacheConfig / BudgetConfig validation (fusion.py:61-67, budget.py:19-24)
+  if (!(cfg->tau_mig >= 0.0 && cfg->tau_mig <= 1.0)) return FC_EINVAL;
+  if (!std::isfinite(cfg->edge_lambda)) return FC_EINVAL;
+  if (!(0.0 <= cfg->alpha_min && cfg->alpha_min <= cfg->alpha_max && cfg->alpha_max <= 1.0)) return FC_EINVAL;
+  return FC_OK;
+}
+
+// Launch sequence of one select step.  `ev` (optional): records an event
+// after every launch, kernel kind in `kind` (0..3) for per-kernel timing.
+struct Recorder {
+  cudaEvent_t* ev = nullptr;
+  int* kind = nullptr;
+  int n = 0, cap = 0;
+  void mark(cudaStream_t st, int k) {
+    if (ev && n < cap) {
+      cudaEventRecord(ev[n], st);
+      kind[n] = k;
+      ++n;
+    }
+  }
+};
+
+void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, const KParams& kp,
+                   const fc_select_out& out, cudaStream_t st, Recorder* rec) {
+  const int B = pl->g.batch;
+  if (pl->fast) {
+    // Chunks of `chunk` streams run A -> B -> C on `lanes` internal streams
+    // (each lane owns its T1/T2 slice) so one chunk's tail overlaps the next
+    // chunk's head; the caller stream forks to and joins from the lanes.
+    // Profiling runs the chunks serially on the caller stream.
+    auto fa = (void (*)(KParams, Dct14, const void*, int, int))sel_fast_rows_fwd(pl->g.format);
+    const int nl = rec ? 1 : pl->lanes;
+    if (!rec) {
+      cudaEventRecord(pl->fork, st);
+      for (int l = 0; l < nl; ++l) cudaStreamWaitEvent(pl->lane[l], pl->fork, 0);
+    }
+    int c = 0;
+    for (int b0 = 0; b0 < B; b0 += pl->chunk, ++c) {
+      const int nb = B - b0 < pl->chunk ? B - b0 : pl->chunk;
+      const int l = c % nl;
+      const cudaStream_t ls = rec ? st : pl->lane[l];
+      KParams kl = kp;
+      kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride);
+      kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
+      fa<<<dim3(32, nb), 448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1);
+      if (rec) rec->mark(st, 0);
+      k448_cols<<<dim3(28, nb), 512, pl->smemB, ls>>>(kl, b0);
+      if (rec) rec->mark(st, 1);
+      k448_rows_inv<<<dim3(28, nb), 512, pl->smemC, ls>>>(kl, b0);
+      if (rec) rec->mark(st, 2);
+    }
+    if (!rec) {
+      for (int l = 0; l < nl; ++l) {
+        cudaEventRecord(pl->join[l], pl->lane[l]);
+        cudaStreamWaitEvent(st, pl->join[l], 0);
+      }
+    }
+  } else {
+    const dim3 blk(FC_THREADS);
+    auto fa = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
+    fa<<<dim3(kp.rows, B), blk, pl->smemA, st>>>(kp, frames, 1);
+    if (rec) rec->mark(st, 0);
+    auto fb = (void (*)(KParams))sel_cols(pl->kh);
+    fb<<<dim3(kp.NCB, B), blk, pl->smemB, st>>>(kp);
+    if (rec) rec->mark(st, 1);
+    auto fc = (void (*)(KParams))sel_rows_inv(pl->kw);
+    fc<<<dim3(kp.NRG, B), blk, pl->smemC, st>>>(kp);
+    if (rec) rec->mark(st, 2);
+  }
+  k_select<<<B, FC_SEL_THREADS, pl->smemD, st>>>(kp, cfg, out);
+  if (rec) rec->mark(st, 3);
 }
 
 }  // namespace
@@ -148,27 +262,46 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
   kp.RG = H >= 16 ? 16 : (H + (H & 1));
   kp.NRG = (H + kp.RG - 1) / kp.RG;
   if (!factor(W, kp.planW) || !factor(H, kp.planH)) { delete pl; return FC_EUNSUPPORTED; }
+  pl->fast = (H == 448 && W == 448 && P == 14);
   pl->kw = (W == 448 || W == 224) ? W : 0;
   pl->kh = (H == 448 || H == 224) ? H : 0;
+  const size_t B = g.batch;
 
-  const int maxpairC = (kp.RG + 1) / 2;
-  pl->smemA = (size_t)P * W * 8 + (size_t)kp.npairA * W * 8 + (size_t)W * 8 + (size_t)kp.cut * P * 8;
-  pl->smemB = (size_t)2 * H * FC_CB * 8 + (size_t)H * 8;
-  pl->smemC = (size_t)2 * maxpairC * W * 8 + (size_t)W * 8;
   int NP2 = 1;
   while (NP2 < N) NP2 <<= 1;
   pl->smemD = (size_t)N * 8 + (size_t)NP2 * 8 + (size_t)NP2 * 4 + (size_t)N * 4 + (size_t)N * 2;
+  size_t specElems, off = 0;
+  if (pl->fast) {
+    const int want = env_int("FC_CHUNK", kChunkDefault, 1, 4096);
+    pl->chunk = (int)(B < (size_t)want ? B : (size_t)want);
+    const int nchunks = (int)((B + pl->chunk - 1) / pl->chunk);
+    pl->lanes = env_int("FC_LANES", kLanesDefault, 1, kMaxLanes);
+    if (pl->lanes > nchunks) pl->lanes = nchunks;
+    pl->smemA = (size_t)kPxBytes448 + (size_t)7 * 448 * sizeof(float2);
+    pl->smemB = (size_t)kScratchB + kStBlock + (size_t)2 * 448 * sizeof(float2);
+    pl->smemC = (size_t)(8 * f448::XR) * sizeof(float2);
+    const size_t ch = pl->chunk;
+    const size_t t1 = align_up(ch * 28 * 448 * 8 * sizeof(float2));
+    const size_t t2 = align_up(ch * 448 * 224 * sizeof(float2));
+    pl->lane_stride = t1 + t2;
+    pl->off_T = off;
+    pl->off_T2 = off + t1;
+    off += pl->lane_stride * pl->lanes;
+    specElems = B * 28 * 512 * 8;  // register-order state
+  } else {
+    pl->chunk = g.batch;
+    const int maxpairC = (kp.RG + 1) / 2;
+    pl->smemA = (size_t)P * W * 8 + (size_t)kp.npairA * W * 8 + (size_t)W * 8 + (size_t)kp.cut * P * 8;
+    pl->smemB = (size_t)2 * H * FC_CB * 8 + (size_t)H * 8;
+    pl->smemC = (size_t)2 * maxpairC * W * 8 + (size_t)W * 8;
+    specElems = B * kp.NCB * (size_t)H * FC_CB;
+    pl->off_T = off; off = align_up(off + specElems * sizeof(float2));
+  }
   const size_t kMaxSmem = 227 * 1024;
   if (pl->smemA > kMaxSmem || pl->smemB > kMaxSmem || pl->smemC > kMaxSmem || pl->smemD > kMaxSmem) {
     delete pl;
     return FC_EUNSUPPORTED;
   }
-
-  // workspace carve
-  const size_t B = g.batch;
-  const size_t specElems = B * kp.NCB * (size_t)H * FC_CB;
-  size_t off = 0;
-  pl->off_T = off; off = align_up(off + specElems * sizeof(float2));
   pl->off_stripes = off; off = align_up(off + B * rows * sizeof(StripeStat));
   pl->off_stats = off; off = align_up(off + B * kp.NCB * 4 * sizeof(double));
   pl->off_peaks = off; off = align_up(off + B * kp.NRG * sizeof(PeakPart));
@@ -185,20 +318,44 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
       const double s = u == 0 ? std::sqrt(1.0 / P) : std::sqrt(2.0 / P);
       dct[(size_t)u * P + x] = s * std::cos(M_PI * u * (2 * x + 1) / (2.0 * P));
     }
+  std::vector<float2> t448(6 * 64), t64(7 * 8);
+  for (int k1 = 1; k1 < 7; ++k1)
+    for (int n2 = 0; n2 < 64; ++n2) t448[(k1 - 1) * 64 + n2] = root((long long)n2 * k1, 448);
+  for (int m2 = 1; m2 < 8; ++m2)
+    for (int j1 = 0; j1 < 8; ++j1) t64[(m2 - 1) * 8 + j1] = root((long long)m2 * j1, 64);
+  if (pl->fast)
+    for (int u = 0; u < 3; ++u)
+      for (int x = 0; x < 14; ++x) pl->dct14.c[u][x] = dct[(size_t)u * 14 + x];
+
   int rc = FC_OK;
-  if (cudaMalloc(&pl->d_twW, W * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc(&pl->d_twH, H * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc(&pl->d_dct, dct.size() * sizeof(double)) != cudaSuccess)
-    rc = FC_ECUDA;
-  if (rc == FC_OK &&
-      (cudaMemcpy(pl->d_twW, tw.data(), W * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess ||
-       cudaMemcpy(pl->d_twH, th.data(), H * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess ||
-       cudaMemcpy(pl->d_dct, dct.data(), dct.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess))
-    rc = FC_ECUDA;
+  auto up = [&](void** dst, const void* src, size_t bytes) {
+    if (rc != FC_OK) return;
+    if (cudaMalloc(dst, bytes) != cudaSuccess || cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = FC_ECUDA;
+  };
+  up((void**)&pl->d_twW, tw.data(), W * sizeof(float2));
+  up((void**)&pl->d_twH, th.data(), H * sizeof(float2));
+  up((void**)&pl->d_dct, dct.data(), dct.size() * sizeof(double));
+  up((void**)&pl->d_tw448, t448.data(), t448.size() * sizeof(float2));
+  up((void**)&pl->d_tw64, t64.data(), t64.size() * sizeof(float2));
+  if (rc == FC_OK && pl->fast) {
+    if (cudaEventCreateWithFlags(&pl->fork, cudaEventDisableTiming) != cudaSuccess) rc = FC_ECUDA;
+    for (int l = 0; l < pl->lanes && rc == FC_OK; ++l) {
+      if (cudaStreamCreateWithFlags(&pl->lane[l], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&pl->join[l], cudaEventDisableTiming) != cudaSuccess)
+        rc = FC_ECUDA;
+    }
+  }
   if (rc == FC_OK) {
-    rc = set_smem(sel_rows_fwd(pl->kw), pl->smemA);
-    if (rc == FC_OK) rc = set_smem(sel_cols(pl->kh), pl->smemB);
-    if (rc == FC_OK) rc = set_smem(sel_rows_inv(pl->kw), pl->smemC);
+    if (pl->fast) {
+      rc = set_smem(sel_fast_rows_fwd(g.format), pl->smemA);
+      if (rc == FC_OK) rc = set_smem((void*)k448_cols, pl->smemB);
+      if (rc == FC_OK) rc = set_smem((void*)k448_rows_inv, pl->smemC);
+    } else {
+      rc = set_smem(sel_rows_fwd(pl->kw), pl->smemA);
+      if (rc == FC_OK) rc = set_smem(sel_cols(pl->kh), pl->smemB);
+      if (rc == FC_OK) rc = set_smem(sel_rows_inv(pl->kw), pl->smemC);
+    }
     if (rc == FC_OK) rc = set_smem((void*)k_select, pl->smemD);
   }
   if (rc != FC_OK) {
@@ -208,6 +365,8 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
   kp.twW = pl->d_twW;
   kp.twH = pl->d_twH;
   kp.dct = pl->d_dct;
+  kp.tw448 = pl->d_tw448;
+  kp.tw64 = pl->d_tw64;
   *out = pl;
   return FC_OK;
 }
@@ -217,6 +376,13 @@ void fc_plan_destroy(fc_plan* pl) {
   if (pl->d_twW) cudaFree(pl->d_twW);
   if (pl->d_twH) cudaFree(pl->d_twH);
   if (pl->d_dct) cudaFree(pl->d_dct);
+  if (pl->d_tw448) cudaFree(pl->d_tw448);
+  if (pl->d_tw64) cudaFree(pl->d_tw64);
+  for (int l = 0; l < kMaxLanes; ++l) {
+    if (pl->lane[l]) cudaStreamDestroy(pl->lane[l]);
+    if (pl->join[l]) cudaEventDestroy(pl->join[l]);
+  }
+  if (pl->fork) cudaEventDestroy(pl->fork);
   delete pl;
 }
 
@@ -232,48 +398,56 @@ int fc_state_reset(const fc_plan* pl, void* state, int32_t first, int32_t count,
   return launch_check();
 }
 
-int fc_select_stage(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
-                    const fc_select_out* out, int32_t stage, void* stream) {
+int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
+              const fc_select_out* out, void* stream) {
   if (!pl || !cfg || !frames || !state || !ws || !out) return FC_EINVAL;
-  if (stage < -1 || stage > 3) return FC_EINVAL;
-  // CacheConfig / BudgetConfig validation (fusion.py:61-67, budget.py:19-24)
-  if (!(cfg->tau_mig >= 0.0 && cfg->tau_mig <= 1.0)) return FC_EINVAL;
-  if (!std::isfinite(cfg->edge_lambda)) return FC_EINVAL;
-  if (!(0.0 <= cfg->alpha_min && cfg->alpha_min <= cfg->alpha_max && cfg->alpha_max <= 1.0)) return FC_EINVAL;
-  const cudaStream_t st = as_stream(stream);
+  const int rc = check_cfg(cfg);
+  if (rc != FC_OK) return rc;
   const KParams kp = bind(pl, state, ws, out->energy);
-  const int B = pl->g.batch;
-  const dim3 blk(FC_THREADS);
-  if (stage < 0 || stage == 0) {
-    const dim3 grid(kp.rows, B);
-    auto fn = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
-    fn<<<grid, blk, pl->smemA, st>>>(kp, frames, 1);
-  }
-  if (stage < 0 || stage == 1) {
-    const dim3 grid(kp.NCB, B);
-    auto fn = (void (*)(KParams))sel_cols(pl->kh);
-    fn<<<grid, blk, pl->smemB, st>>>(kp);
-  }
-  if (stage < 0 || stage == 2) {
-    const dim3 grid(kp.NRG, B);
-    auto fn = (void (*)(KParams))sel_rows_inv(pl->kw);
-    fn<<<grid, blk, pl->smemC, st>>>(kp);
-  }
-  if (stage < 0 || stage == 3) k_select<<<B, FC_SEL_THREADS, pl->smemD, st>>>(kp, *cfg, *out);
+  launch_select(pl, *cfg, frames, kp, *out, as_stream(stream), nullptr);
   return launch_check();
 }
 
-int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
-              const fc_select_out* out, void* stream) {
-  return fc_select_stage(pl, cfg, frames, state, ws, out, -1, stream);
+int fc_select_profile(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
+                      const fc_select_out* out, float* kernel_ms, void* stream) {
+  if (!pl || !cfg || !frames || !state || !ws || !out || !kernel_ms) return FC_EINVAL;
+  int rc = check_cfg(cfg);
+  if (rc != FC_OK) return rc;
+  const cudaStream_t st = as_stream(stream);
+  const KParams kp = bind(pl, state, ws, out->energy);
+  const int cap = 3 * ((pl->g.batch + pl->chunk - 1) / pl->chunk) + 2;  // serial chunks
+  std::vector<cudaEvent_t> ev(cap);
+  std::vector<int> kind(cap);
+  for (auto& e : ev) cudaEventCreate(&e);
+  Recorder r;
+  r.ev = ev.data();
+  r.kind = kind.data();
+  r.cap = cap;
+  r.mark(st, -1);
+  launch_select(pl, *cfg, frames, kp, *out, st, &r);
+  rc = launch_check();
+  cudaStreamSynchronize(st);
+  for (int k = 0; k < 4; ++k) kernel_ms[k] = 0.f;
+  for (int i = 1; i < r.n; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+    if (kind[i] >= 0 && kind[i] < 4) kernel_ms[kind[i]] += ms;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
 }
 
 int fc_patch_energy(const fc_plan* pl, const void* frames, void* ws, double* energy, void* stream) {
   if (!pl || !frames || !ws || !energy) return FC_EINVAL;
   const KParams kp = bind(pl, nullptr, ws, energy);
-  const dim3 grid(kp.rows, pl->g.batch);
-  auto fn = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
-  fn<<<grid, FC_THREADS, pl->smemA, as_stream(stream)>>>(kp, frames, 0);
+  const cudaStream_t st = as_stream(stream);
+  if (pl->fast) {
+    auto fn = (void (*)(KParams, Dct14, const void*, int, int))sel_fast_rows_fwd(pl->g.format);
+    fn<<<dim3(32, pl->g.batch), 448, pl->smemA, st>>>(kp, pl->dct14, frames, 0, 0);
+  } else {
+    auto fn = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
+    fn<<<dim3(kp.rows, pl->g.batch), FC_THREADS, pl->smemA, st>>>(kp, frames, 0);
+  }
   return launch_check();
 }
 

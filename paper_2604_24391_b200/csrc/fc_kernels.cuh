@@ -31,10 +31,15 @@
 #define FC_MAX_TOKENS 4096
 #define FC_MAX_PATCH 32
 
+// Per-stripe frame flags.  A frame is constant iff no stripe varies and all
+// stripes share `ref`; it is all-zero iff constant with ref == 0
+// (fusion.py:147 np.ptp == 0; migration.py:103 zero norm).
 struct StripeStat {
-  double mn, mx;
-  int32_t nonfinite;
-  int32_t pad[3];
+  double ref;         // one pixel value of the stripe
+  double unused;
+  int32_t nonfinite;  // any pixel NaN/Inf (frame.py:13)
+  int32_t varying;    // some pixel differs from ref
+  int32_t pad[2];
 };
 
 struct PeakPart {
@@ -58,7 +63,10 @@ struct KParams {
   const float2* twW;
   const float2* twH;
   const double* dct;  // [cut][P] orthonormal DCT-II rows u < cut
+  const float2* tw448;  // fast path: w448^{n2 k1}, [6][64]
+  const float2* tw64;   // fast path: w64^{m2 j1},  [7][8]
   float2* T;
+  float2* T2;           // fast path: inverse-column output, [chunk][448][224]
   StripeStat* stripes;
   double* stats;  // [B][NCB][4]
   PeakPart* peaks;
@@ -242,7 +250,8 @@ __global__ void __launch_bounds__(FC_THREADS) k_rows_fwd(KParams kp, const void*
         mn = fmin(mn, red[w * 3]); mx = fmax(mx, red[w * 3 + 1]); bad = fmax(bad, red[w * 3 + 2]);
       }
       StripeStat st;
-      st.mn = mn; st.mx = mx; st.nonfinite = bad != 0.0; st.pad[0] = st.pad[1] = st.pad[2] = 0;
+      st.ref = mn; st.unused = mx; st.nonfinite = bad != 0.0; st.varying = mn != mx;
+      st.pad[0] = st.pad[1] = 0;
       kp.stripes[(size_t)b * kp.rows + s] = st;
     }
   }
@@ -539,17 +548,62 @@ __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config
   const double* energy = kp.energy + (size_t)b * N;
   for (int p = threadIdx.x; p < N; p += blockDim.x) E[p] = energy[p];
 
+  __shared__ double sh_sum[4], sh_ref;
+  __shared__ int sh_bad, sh_vary, sh_pos;
+  __shared__ float sh_pv, sh_pv2;
+  if (threadIdx.x < 32) {
+    // warp 0 gathers the per-CTA partials of K_A/K_B/K_C (fixed-order trees)
+    const int lane = threadIdx.x;
+    const double ref0 = kp.stripes[(size_t)b * kp.rows].ref;
+    int bad = 0, vary = 0;
+    for (int s = lane; s < kp.rows; s += 32) {
+      const StripeStat st = kp.stripes[(size_t)b * kp.rows + s];
+      bad |= st.nonfinite;
+      vary |= st.varying | (st.ref != ref0);
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int c = lane; c < kp.NCB; c += 32) {
+      const double* st = kp.stats + ((size_t)b * kp.NCB + c) * 4;
+      a0 += st[0]; a1 += st[1]; a2 += st[2]; a3 += st[3];
+    }
+    PeakKey bk = {-CUDART_INF_F, 0x7fffffff, 0x7fffffff};
+    float v2 = -CUDART_INF_F;
+    for (int g = lane; g < kp.NRG; g += 32) {
+      const PeakPart o = kp.peaks[(size_t)b * kp.NRG + g];
+      const PeakKey ok = {o.v, abs(canon_disp(o.y, kp.H)) + abs(canon_disp(o.j, kp.W)), o.y * kp.W + o.j};
+      if (peak_better(ok, bk)) { v2 = fmaxf(fmaxf(v2, o.v2), bk.v); bk = ok; }
+      else v2 = fmaxf(fmaxf(v2, o.v2), ok.v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+      vary |= __shfl_xor_sync(0xffffffffu, vary, o);
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+      a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+      PeakKey ok;
+      ok.v = __shfl_xor_sync(0xffffffffu, bk.v, o);
+      ok.l1 = __shfl_xor_sync(0xffffffffu, bk.l1, o);
+      ok.pos = __shfl_xor_sync(0xffffffffu, bk.pos, o);
+      const float ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+      if (peak_better(ok, bk)) { v2 = fmaxf(fmaxf(v2, ov2), bk.v); bk = ok; }
+      else v2 = fmaxf(fmaxf(v2, ov2), ok.v);
+    }
+    if (lane == 0) {
+      sh_ref = ref0; sh_vary = vary; sh_bad = bad;
+      sh_sum[0] = a0; sh_sum[1] = a1; sh_sum[2] = a2; sh_sum[3] = a3;
+      sh_pv = bk.v; sh_pv2 = v2; sh_pos = bk.pos;
+    }
+  }
+  __syncthreads();
+
   if (threadIdx.x == 0) {
     StreamHdr h = kp.hdr[b];
     // frame flags (fusion.py:147, frame.py:13)
-    double mn = CUDART_INF, mx = -CUDART_INF;
-    int bad = 0;
-    for (int s = 0; s < kp.rows; ++s) {
-      const StripeStat st = kp.stripes[(size_t)b * kp.rows + s];
-      mn = fmin(mn, st.mn); mx = fmax(mx, st.mx); bad |= st.nonfinite;
-    }
-    const int czero = (mn == 0.0 && mx == 0.0);
-    const int cconst = (mn == mx);
+    const int bad = sh_bad;
+    const int cconst = !sh_vary;
+    const int czero = cconst && sh_ref == 0.0;
     memset(&R, 0, sizeof(R));
     R.rows = kp.rows; R.cols = kp.cols;
     R.bin_count = (int64_t)kp.H * kp.W;
@@ -558,11 +612,7 @@ __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config
     R.cold = cold;
     int flush = 1, dip = 0, djp = 0;
     if (!cold && !bad) {
-      double spc = 0, spp = 0, scc = 0, splp = 0;
-      for (int c = 0; c < kp.NCB; ++c) {
-        const double* st = kp.stats + ((size_t)b * kp.NCB + c) * 4;
-        spc += st[0]; spp += st[1]; scc += st[2]; splp += st[3];
-      }
+      const double spc = sh_sum[0], spp = sh_sum[1], scc = sh_sum[2], splp = sh_sum[3];
       // Module I (migration.py:87-105, fusion.py:147-150)
       int mig = FC_DIAG_NONE;
       if (h.prev_zero || czero) mig = FC_DIAG_DEGENERATE;
@@ -570,22 +620,11 @@ __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config
       if (mig == FC_DIAG_NONE) {
         double sim = spc / (sqrt(spp) * sqrt(scc));
         R.sim_freq = sim < 1.0 ? sim : 1.0;
-        PeakPart best = kp.peaks[(size_t)b * kp.NRG];
-        PeakKey bk = {best.v, abs(canon_disp(best.y, kp.H)) + abs(canon_disp(best.j, kp.W)),
-                      best.y * kp.W + best.j};
-        float v2 = best.v2;
-        for (int g = 1; g < kp.NRG; ++g) {
-          const PeakPart o = kp.peaks[(size_t)b * kp.NRG + g];
-          const PeakKey ok = {o.v, abs(canon_disp(o.y, kp.H)) + abs(canon_disp(o.j, kp.W)),
-                              o.y * kp.W + o.j};
-          if (peak_better(ok, bk)) { v2 = fmaxf(fmaxf(v2, o.v2), bk.v); bk = ok; best = o; }
-          else v2 = fmaxf(fmaxf(v2, o.v2), ok.v);
-        }
         const double inv_hw = 1.0 / ((double)kp.H * kp.W);
-        R.peak = (double)bk.v * inv_hw;
-        R.peak_runner_up = (double)v2 * inv_hw;
-        R.di = canon_disp(best.y, kp.H);
-        R.dj = canon_disp(best.j, kp.W);
+        R.peak = (double)sh_pv * inv_hw;
+        R.peak_runner_up = (double)sh_pv2 * inv_hw;
+        R.di = canon_disp(sh_pos / kp.W, kp.H);
+        R.dj = canon_disp(sh_pos % kp.W, kp.W);
         R.di_patches = to_patch_units(R.di, kp.P);
         R.dj_patches = to_patch_units(R.dj, kp.P);
         dip = R.di_patches; djp = R.dj_patches;

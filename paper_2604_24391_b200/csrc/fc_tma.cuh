@@ -1,0 +1,55 @@
+// Bulk asynchronous global->shared copies (TMA engine, cp.async.bulk) with
+// mbarrier completion, for staging contiguous tiles: frame stripes, spectrum
+// column blocks and per-stream state blocks.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// One thread initialises; caller must __syncthreads() afterwards.
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Arm the barrier for `bytes` of transactions (one arrival).
+__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+// Bulk copy of `bytes` (multiple of 16, both addresses 16-byte aligned).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Copy a large contiguous tile in <= 32 KB pieces on one barrier.
+__device__ __forceinline__ void load_tile(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  bar_expect(bar, bytes);
+  const uint32_t piece = 32768;
+  for (uint32_t off = 0; off < bytes; off += piece) {
+    const uint32_t n = bytes - off < piece ? bytes - off : piece;
+    bulk_g2s(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, n, bar);
+  }
+}
+
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+}  // namespace tma

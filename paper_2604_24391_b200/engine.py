@@ -80,6 +80,10 @@ class FreqCacheEngine:
         self.rows = self.height // self.patch_size
         self.cols = self.width // self.patch_size
         self.n_tokens = self.lib.fc_plan_tokens(plan)
+        fast = (self.height, self.width, self.patch_size) == (448, 448, 14)
+        import os
+        chunk = min(self.batch, max(1, int(os.environ.get("FC_CHUNK", "32"))))
+        self.launches_per_select = (3 * -(-self.batch // chunk) + 1) if fast else 4
         sb = self.lib.fc_plan_state_bytes(plan)
         wb = self.lib.fc_plan_workspace_bytes(plan)
         self.state = torch.zeros(sb, dtype=torch.uint8, device=self.device)
@@ -130,9 +134,10 @@ class FreqCacheEngine:
         if not frames.is_contiguous():
             raise ValueError("frames must be contiguous")
 
-    def select(self, frames, cfg, out=None, refresh_shift=None, stage=-1):
+    def select(self, frames, cfg, out=None, refresh_shift=None, profile=None):
         """One decision step for every stream; returns device outputs.
-        ``stage`` 0..3 launches a single kernel of the step (timing only)."""
+        ``profile``: a list that receives per-kernel device ms (rows_fwd,
+        cols, rows_inv, select) — synchronises; benchmarking only."""
         self._check_frames(frames)
         out = self.out if out is None else out
         so = nat.SelectOut(out.results.data_ptr(), out.reuse_idx.data_ptr(), out.recompute_idx.data_ptr(),
@@ -140,9 +145,14 @@ class FreqCacheEngine:
                            out.energy.data_ptr())
         conf = make_config(cfg, refresh_shift)
         with torch.cuda.device(self.device):
-            rc = self.lib.fc_select_stage(self._plan, C.byref(conf), _ptr(frames), _ptr(self.state),
-                                          _ptr(self.workspace), C.byref(so), int(stage),
-                                          _stream(self.device))
+            if profile is None:
+                rc = self.lib.fc_select(self._plan, C.byref(conf), _ptr(frames), _ptr(self.state),
+                                        _ptr(self.workspace), C.byref(so), _stream(self.device))
+            else:
+                ms = (C.c_float * 4)()
+                rc = self.lib.fc_select_profile(self._plan, C.byref(conf), _ptr(frames), _ptr(self.state),
+                                                _ptr(self.workspace), C.byref(so), ms, _stream(self.device))
+                profile[:] = list(ms)
         nat.check(rc, "fc_select")
         return out
 
