@@ -180,7 +180,7 @@ __device__ void stripe_energy(const double* __restrict__ g, const double* __rest
 template <int NW>
 __global__ void __launch_bounds__(FC_THREADS) k_rows_fwd(KParams kp, const void* __restrict__ frames,
                                                          int do_fft) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double red[32 * 3];
   const int s = blockIdx.x, b = blockIdx.y;
   const int P = kp.P, W = kp.W, H = kp.H;
@@ -338,7 +338,7 @@ __device__ __forceinline__ void unpack_dcny(float2 zk, float2 zm, float2& f0, fl
 
 template <int NH>
 __global__ void __launch_bounds__(FC_THREADS) k_cols(KParams kp) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double red[32 * 4];
   const int cb = blockIdx.x, b = blockIdx.y;
   const int H = kp.H;
@@ -447,7 +447,7 @@ __device__ __forceinline__ bool peak_better(const PeakKey& a, const PeakKey& b) 
 
 template <int NW>
 __global__ void __launch_bounds__(FC_THREADS) k_rows_inv(KParams kp) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ PeakKey redk[32];
   __shared__ float redv[32];
   const int gidx = blockIdx.x, b = blockIdx.y;
@@ -529,7 +529,7 @@ __device__ __forceinline__ bool key_less(double ea, int ia, double eb, int ib) {
 // hold by construction).  Scalars in thread 0, per-token work spread.
 __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config cfg,
                                                            fc_select_out out) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int b = blockIdx.x;
   const int N = kp.N;
   int NP2 = 1;
