@@ -158,6 +158,28 @@ int  fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                int32_t fresh_layout, void* out, int64_t* out_ages,
                void* cuda_stream);
 
+/* ---- stand-alone stage operators on arbitrary fp64 arrays (device pointers).
+ * `ws` is a device scratch buffer of fc_stage_workspace_bytes(); results are
+ * written to device memory; `flags` (device int32): bit0 non-finite input,
+ * bit1 negative amplitude, bit2 candidate index out of range.  Deterministic. */
+int64_t fc_stage_workspace_bytes(void);
+/* sim_freq (migration.py:87-105): out3 = {sum a*b, sum a^2, sum b^2}        */
+int  fc_amp_cosine(const double* a, const double* b, int64_t n, void* ws,
+                   double* out3, int32_t* flags, void* cuda_stream);
+/* spectral_entropy (budget.py:34-58): out2 = {sum P, sum p ln p}, P = a^2,
+ * p = P / sum P, the DC bin (index 0) dropped when include_dc == 0          */
+int  fc_spectral_sums(const double* amp, int64_t n, int32_t include_dc, void* ws,
+                      double* out2, int32_t* flags, void* cuda_stream);
+/* refresh_mask (edge_refresh.py:62-73): mask = e > mean + lam * std
+ * (population), stats3 = {mean, std, threshold}                            */
+int  fc_refresh_mask(const double* energy, int64_t n, double lam, void* ws,
+                     uint8_t* mask, double* stats3, void* cuda_stream);
+/* topk_ascending (fusion.py:104-115): first min(k, m) candidates ordered by
+ * (energies[cand], cand) ascending; m <= 8192                               */
+int  fc_topk_ascending(const int64_t* cand, int64_t m, const double* energies,
+                       int64_t n_energies, int64_t k, int64_t* out,
+                       int32_t* flags, void* cuda_stream);
+
 /* Build src_map for one stream from an ordered reuse list (fusion.py:481-504).
  * flag (device int32, may be NULL) receives FC_EBOUNDS on an out-of-bounds
  * source. */

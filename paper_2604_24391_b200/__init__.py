@@ -45,7 +45,11 @@ from .api import (  # noqa: F401
     patch_energy,
     phase_correlation,
     populate_cache,
+    refresh_mask,
     run_sequence,
+    sim_freq,
+    spectral_entropy,
     step,
+    topk_ascending,
 )
 from .engine import FreqCacheEngine, SelectResult, splice, splice_map  # noqa: F401

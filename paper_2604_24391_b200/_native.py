@@ -41,7 +41,8 @@ EXPORTS = (
     "fc_abi_version", "fc_strerror", "fc_plan_create", "fc_plan_destroy",
     "fc_plan_state_bytes", "fc_plan_workspace_bytes", "fc_plan_tokens",
     "fc_state_reset", "fc_select", "fc_select_profile", "fc_patch_energy", "fc_splice",
-    "fc_splice_map",
+    "fc_splice_map", "fc_stage_workspace_bytes", "fc_amp_cosine", "fc_spectral_sums",
+    "fc_refresh_mask", "fc_topk_ascending",
 )
 
 
@@ -110,6 +111,11 @@ def load(path=None):
         "fc_patch_energy": (C.c_int, [vp, vp, vp, vp, vp]),
         "fc_splice": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, i32, vp, vp, vp]),
         "fc_splice_map": (C.c_int, [i32, i32, vp, i32, i32, i32, vp, vp, vp]),
+        "fc_stage_workspace_bytes": (i64, []),
+        "fc_amp_cosine": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
+        "fc_spectral_sums": (C.c_int, [vp, i64, i32, vp, vp, vp, vp]),
+        "fc_refresh_mask": (C.c_int, [vp, i64, C.c_double, vp, vp, vp, vp]),
+        "fc_topk_ascending": (C.c_int, [vp, i64, vp, i64, i64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -315,3 +315,105 @@ def phase_correlation(prev, curr, patch_size=1):
     if int(res["diagnostic"]) in (nat.FC_DIAG_DEGENERATE, nat.FC_DIAG_NO_TEXTURE):
         raise ConstantFrameError("no texture; displacement undefined")
     return Displacement.from_pixels(int(res["di"]), int(res["dj"]), patch_size)
+
+
+# ------------------------------------------ array stage operators (GPU) ----
+
+def _stage_ws(dev):
+    ws = _STAGE_WS.get(dev)
+    if ws is None:
+        ws = torch.empty(nat.lib().fc_stage_workspace_bytes(), dtype=torch.uint8, device=dev)
+        _STAGE_WS[dev] = ws
+    return ws
+
+
+_STAGE_WS = {}
+
+
+def _dev_f64(a):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)).ravel()).to("cuda")
+
+
+def sim_freq(amp_prev, amp_curr):
+    """Cosine of two amplitude grids, clamped to 1 (migration.py:87-105)."""
+    from .engine import _ptr, _stream
+    from .types import DegenerateSpectrumError
+    a = np.asarray(amp_prev, dtype=np.float64)
+    b = np.asarray(amp_curr, dtype=np.float64)
+    if a.ravel().shape != b.ravel().shape:
+        raise ValueError("amplitude grids must have equal dimensions")
+    lib = nat.lib()
+    ta, tb = _dev_f64(a), _dev_f64(b)
+    out = torch.empty(3, dtype=torch.float64, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.check(lib.fc_amp_cosine(_ptr(ta), _ptr(tb), int(ta.numel()), _ptr(_stage_ws(ta.device)), _ptr(out),
+                                _ptr(flags), _stream(ta.device)), "fc_amp_cosine")
+    f = int(flags.item())
+    if f & 1:
+        raise ValueError("amplitude grids contain non-finite values")
+    if f & 2:
+        raise ValueError("amplitude grids must be nonnegative")
+    dot, n2a, n2b = out.tolist()
+    na, nb = math.sqrt(n2a), math.sqrt(n2b)
+    if na == 0.0 or nb == 0.0:
+        raise DegenerateSpectrumError("degenerate spectrum")
+    return min(1.0, dot / (na * nb))
+
+
+def spectral_entropy(amplitude, include_dc=True):
+    """Normalised Shannon entropy of the power spectrum (budget.py:34-58)."""
+    from .engine import _ptr, _stream
+    from .types import DegenerateSpectrumError
+    a = np.asarray(amplitude, dtype=np.float64)
+    if a.size < 2:
+        raise ValueError("amplitude grid must have at least 2 bins")
+    lib = nat.lib()
+    ta = _dev_f64(a)
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.check(lib.fc_spectral_sums(_ptr(ta), int(ta.numel()), 1 if include_dc else 0, _ptr(_stage_ws(ta.device)),
+                                   _ptr(out), _ptr(flags), _stream(ta.device)), "fc_spectral_sums")
+    f = int(flags.item())
+    if f & 1:
+        raise ValueError("amplitude grid contains non-finite values")
+    if f & 2:
+        raise ValueError("amplitude grid must be nonnegative")
+    total, plogp = out.tolist()
+    if total <= 0.0:
+        raise DegenerateSpectrumError("degenerate spectrum")
+    raw = -plogp + 0.0
+    return EntropyReading(raw, raw / math.log(a.size), a.size)
+
+
+def refresh_mask(energy, sensitivity):
+    """Population mean/std threshold, strict '>' (edge_refresh.py:62-73)."""
+    from .engine import _ptr, _stream
+    from .types import RefreshMask
+    e = np.asarray(energy.energies, dtype=np.float64)
+    lib = nat.lib()
+    te = _dev_f64(e)
+    mask = torch.empty(te.numel(), dtype=torch.uint8, device="cuda")
+    stats = torch.empty(3, dtype=torch.float64, device="cuda")
+    nat.check(lib.fc_refresh_mask(_ptr(te), int(te.numel()), float(sensitivity), _ptr(_stage_ws(te.device)),
+                                  _ptr(mask), _ptr(stats), _stream(te.device)), "fc_refresh_mask")
+    mu, sd, _ = stats.tolist()
+    return RefreshMask(mask.cpu().numpy().astype(bool).reshape(e.shape), mu, sd, float(sensitivity))
+
+
+def topk_ascending(candidates, energies, k):
+    """First k candidates by ascending energy, ties row-major (fusion.py:104-115)."""
+    from .engine import _ptr, _stream
+    cand = np.asarray(candidates, dtype=np.int64).ravel()
+    if cand.size == 0 or k <= 0:
+        return ()
+    lib = nat.lib()
+    e = _dev_f64(energies)
+    tc = torch.from_numpy(cand).to("cuda")
+    kout = min(int(k), cand.size)
+    out = torch.empty(kout, dtype=torch.int64, device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.check(lib.fc_topk_ascending(_ptr(tc), int(cand.size), _ptr(e), int(e.numel()), int(k), _ptr(out),
+                                    _ptr(flags), _stream(tc.device)), "fc_topk_ascending")
+    if int(flags.item()) & 4:
+        raise IndexError("candidate index out of range")
+    return tuple(int(v) for v in out.cpu().tolist())

@@ -19,10 +19,11 @@
 
 #include "fc_kernels.cuh"
 #include "fc_fast448.cuh"
+#include "fc_stages.cuh"
 
 namespace {
-constexpr int kChunkDefault = 32;  // streams per A/B/C launch group on the fast path
-constexpr int kLanesDefault = 2;   // concurrent chunk lanes (internal CUDA streams)
+constexpr int kChunkDefault = 512;  // streams per A/B/C launch group on the fast path
+constexpr int kLanesDefault = 1;   // concurrent chunk lanes (internal CUDA streams)
 constexpr int kMaxLanes = 8;
 
 int env_int(const char* name, int dflt, int lo, int hi) {
@@ -44,6 +45,8 @@ struct fc_plan {
   cudaEvent_t fork = nullptr;
   cudaEvent_t join[kMaxLanes] = {};
   size_t lane_stride = 0;              // workspace bytes per lane (T1 + T2)
+  bool persistent = false;             // fast path: persistent K_B / K_C (FC_PERSISTENT=1)
+  int gridB = 0, gridC = 0;            // persistent grid sizes (SMs x occupancy)
   float2* d_twW = nullptr;
   float2* d_twH = nullptr;
   double* d_dct = nullptr;
@@ -189,9 +192,19 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
       fa<<<dim3(32, nb), 448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1);
       if (rec) rec->mark(st, 0);
-      k448_cols<<<dim3(28, nb), 512, pl->smemB, ls>>>(kl, b0);
+      if (pl->persistent) {
+        const int gb = nb * kNCB448 < pl->gridB ? nb * kNCB448 : pl->gridB;
+        k448_cols_p<<<gb, 64 * kBC, kSmemBP, ls>>>(kl, b0, nb);
+      } else {
+        k448_cols<<<dim3(kNCB448, nb), 64 * kBC, pl->smemB, ls>>>(kl, b0);
+      }
       if (rec) rec->mark(st, 1);
-      k448_rows_inv<<<dim3(28, nb), 512, pl->smemC, ls>>>(kl, b0);
+      if (pl->persistent) {
+        const int gc = nb * kNRG448 < pl->gridC ? nb * kNRG448 : pl->gridC;
+        k448_rows_inv_p<<<gc, 64 * kBP, kSmemCP, ls>>>(kl, b0, nb);
+      } else {
+        k448_rows_inv<<<dim3(kNRG448, nb), 64 * kBP, pl->smemC, ls>>>(kl, b0);
+      }
       if (rec) rec->mark(st, 2);
     }
     if (!rec) {
@@ -279,15 +292,17 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     if (pl->lanes > nchunks) pl->lanes = nchunks;
     pl->smemA = (size_t)kPxBytes448 + (size_t)7 * 448 * sizeof(float2);
     pl->smemB = (size_t)kScratchB + kStBlock + (size_t)2 * 448 * sizeof(float2);
-    pl->smemC = (size_t)(8 * f448::XR) * sizeof(float2);
+    pl->smemC = (size_t)(kBP * f448::XR) * sizeof(float2);
+    kp.NCB = kNCB448;   // K_B stats partials per stream
+    kp.NRG = kNRG448;   // K_C peak partials per stream
     const size_t ch = pl->chunk;
-    const size_t t1 = align_up(ch * 28 * 448 * 8 * sizeof(float2));
+    const size_t t1 = align_up(ch * 224 * 448 * sizeof(float2));
     const size_t t2 = align_up(ch * 448 * 224 * sizeof(float2));
     pl->lane_stride = t1 + t2;
     pl->off_T = off;
     pl->off_T2 = off + t1;
     off += pl->lane_stride * pl->lanes;
-    specElems = B * 28 * 512 * 8;  // register-order state
+    specElems = B * kNCB448 * 64 * kBC * 8;  // register-order state
   } else {
     pl->chunk = g.batch;
     const int maxpairC = (kp.RG + 1) / 2;
@@ -351,6 +366,18 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
       rc = set_smem(sel_fast_rows_fwd(g.format), pl->smemA);
       if (rc == FC_OK) rc = set_smem((void*)k448_cols, pl->smemB);
       if (rc == FC_OK) rc = set_smem((void*)k448_rows_inv, pl->smemC);
+      if (rc == FC_OK) rc = set_smem((void*)k448_cols_p, kSmemBP);
+      if (rc == FC_OK) rc = set_smem((void*)k448_rows_inv_p, kSmemCP);
+      if (rc == FC_OK) {
+        int dev = 0, sms = 148, ob = 0, oc = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k448_cols_p, 64 * kBC, kSmemBP);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k448_rows_inv_p, 64 * kBP, kSmemCP);
+        pl->gridB = sms * (ob > 0 ? ob : 1);
+        pl->gridC = sms * (oc > 0 ? oc : 1);
+        pl->persistent = env_int("FC_PERSISTENT", 0, 0, 1) != 0;
+      }
     } else {
       rc = set_smem(sel_rows_fwd(pl->kw), pl->smemA);
       if (rc == FC_OK) rc = set_smem(sel_cols(pl->kh), pl->smemB);
@@ -495,6 +522,77 @@ int fc_splice_map(int32_t rows, int32_t cols, const int32_t* reuse_idx, int32_t 
       return FC_ECUDA;
   }
   k_splice_map<<<1, 512, smem, as_stream(stream)>>>(rows, cols, reuse_idx, k, dip, djp, src_map, flag);
+  return launch_check();
+}
+
+// ---------------------------------------------------------- stage ops ----
+
+static int stage_blocks(int64_t n) {
+  int64_t nb = (n + 1023) / 1024;
+  if (nb < 1) nb = 1;
+  if (nb > FC_STAGE_BLOCKS) nb = FC_STAGE_BLOCKS;
+  return (int)nb;
+}
+
+int64_t fc_stage_workspace_bytes(void) { return FC_STAGE_WS_BYTES; }
+
+// ws layout: [flags int32 | pad][out scratch 8 doubles][partials 4*FC_STAGE_BLOCKS doubles]
+int fc_amp_cosine(const double* a, const double* b, int64_t n, void* ws, double* out3, int32_t* flags,
+                  void* stream) {
+  if (!a || !b || n < 1 || !ws || !out3 || !flags) return FC_EINVAL;
+  const cudaStream_t st = as_stream(stream);
+  double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 128);
+  const int nb = stage_blocks(n);
+  cudaMemsetAsync(flags, 0, sizeof(int32_t), st);
+  stg::k_cos_part<<<nb, FC_STAGE_THREADS, 0, st>>>(a, b, n, part, flags);
+  stg::k_final<3><<<1, FC_STAGE_THREADS, 0, st>>>(part, nb, out3, 1.0);
+  return launch_check();
+}
+
+int fc_spectral_sums(const double* amp, int64_t n, int32_t include_dc, void* ws, double* out2, int32_t* flags,
+                     void* stream) {
+  if (!amp || n < 1 || !ws || !out2 || !flags) return FC_EINVAL;
+  const cudaStream_t st = as_stream(stream);
+  double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 128);
+  const int nb = stage_blocks(n);
+  cudaMemsetAsync(flags, 0, sizeof(int32_t), st);
+  stg::k_pow_part<<<nb, FC_STAGE_THREADS, 0, st>>>(amp, n, include_dc, part, flags);
+  stg::k_final<1><<<1, FC_STAGE_THREADS, 0, st>>>(part, nb, out2, 1.0);
+  stg::k_plogp_part<<<nb, FC_STAGE_THREADS, 0, st>>>(amp, n, include_dc, out2, part);
+  stg::k_final<1><<<1, FC_STAGE_THREADS, 0, st>>>(part, nb, out2 + 1, 1.0);
+  return launch_check();
+}
+
+int fc_refresh_mask(const double* energy, int64_t n, double lam, void* ws, uint8_t* mask, double* stats3,
+                    void* stream) {
+  if (!energy || n < 1 || !ws || !mask || !stats3) return FC_EINVAL;
+  const cudaStream_t st = as_stream(stream);
+  double* sc = reinterpret_cast<double*>(static_cast<char*>(ws) + 64);  // [mean, m2]
+  double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + 128);
+  const int nb = stage_blocks(n);
+  stg::k_moment_part<<<nb, FC_STAGE_THREADS, 0, st>>>(energy, n, nullptr, part);
+  stg::k_final<1><<<1, FC_STAGE_THREADS, 0, st>>>(part, nb, sc, (double)n, energy);
+  stg::k_moment_part<<<nb, FC_STAGE_THREADS, 0, st>>>(energy, n, sc, part);
+  stg::k_final<1><<<1, FC_STAGE_THREADS, 0, st>>>(part, nb, sc + 1, (double)n);
+  const int tb = (int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+  stg::k_threshold<<<tb, 256, 0, st>>>(energy, n, sc, lam, mask, stats3);
+  return launch_check();
+}
+
+int fc_topk_ascending(const int64_t* cand, int64_t m, const double* energies, int64_t n_energies, int64_t k,
+                      int64_t* out, int32_t* flags, void* stream) {
+  if (m < 0 || (m > 0 && (!cand || !energies || !out || !flags))) return FC_EINVAL;
+  if (m == 0 || k <= 0) return FC_OK;
+  if (m > 8192) return FC_EUNSUPPORTED;
+  int np2 = 1;
+  while (np2 < m) np2 <<= 1;
+  const size_t smem = (size_t)np2 * 16;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute((void*)stg::k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return FC_ECUDA;
+  const cudaStream_t st = as_stream(stream);
+  cudaMemsetAsync(flags, 0, sizeof(int32_t), st);
+  stg::k_topk<<<1, 1024, smem, st>>>(cand, (int)m, energies, n_energies, k, out, flags);
   return launch_check();
 }
 

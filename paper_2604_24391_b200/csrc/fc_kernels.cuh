@@ -90,8 +90,10 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-// Deterministic block sum of NV doubles; result valid in thread 0.
-template <int NV>
+// Deterministic block sum of NV doubles; result valid in thread 0.  Warp
+// xor-trees, then warp 0 reduces the per-warp partials with another fixed
+// tree (no serial tail).  SYNC_AFTER: trailing barrier (scratch reuse).
+template <int NV, bool SYNC_AFTER = true>
 __device__ __forceinline__ void block_sum_d(double (&v)[NV], double* scratch /* 32*NV */) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
@@ -100,15 +102,34 @@ __device__ __forceinline__ void block_sum_d(double (&v)[NV], double* scratch /* 
 #pragma unroll
     for (int i = 0; i < NV; ++i) scratch[wid * NV + i] = v[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (wid == 0) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += scratch[w * NV + i];
-      v[i] = s;
+      double s = lane < nw ? scratch[lane * NV + i] : 0.0;
+      v[i] = warp_sum(s);
     }
   }
+  if (SYNC_AFTER) __syncthreads();
+}
+
+// fp32 per-thread partials -> fp32 warp trees -> fp64 across warps.
+template <int NV>
+__device__ __forceinline__ void block_sum_f2d(const float (&f)[NV], double (&v)[NV], double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float w[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) w[i] = warp_sum(f[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[wid * NV + i] = (double)w[i];
   __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double s = lane < nw ? scratch[lane * NV + i] : 0.0;
+      v[i] = warp_sum(s);
+    }
+  }
 }
 
 __device__ __forceinline__ int canon_disp(int pos, int n) {
@@ -673,11 +694,13 @@ __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config
 
   // Module II statistics (edge_refresh.py:62-73): population mean / std
   double s1 = 0.0;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) s1 += E[p];
+  // shifted by E[0]: an all-equal energy map keeps an exact mean and std 0
+  const double e0 = E[0];
+  for (int p = threadIdx.x; p < N; p += blockDim.x) s1 += E[p] - e0;
   {
     double v[1] = {s1};
     block_sum_d<1>(v, red);
-    if (threadIdx.x == 0) red[63] = v[0] / (double)N;
+    if (threadIdx.x == 0) red[63] = e0 + v[0] / (double)N;
   }
   __syncthreads();
   const double mu = red[63];

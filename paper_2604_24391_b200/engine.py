@@ -82,7 +82,7 @@ class FreqCacheEngine:
         self.n_tokens = self.lib.fc_plan_tokens(plan)
         fast = (self.height, self.width, self.patch_size) == (448, 448, 14)
         import os
-        chunk = min(self.batch, max(1, int(os.environ.get("FC_CHUNK", "32"))))
+        chunk = min(self.batch, max(1, int(os.environ.get("FC_CHUNK", "512"))))
         self.launches_per_select = (3 * -(-self.batch // chunk) + 1) if fast else 4
         sb = self.lib.fc_plan_state_bytes(plan)
         wb = self.lib.fc_plan_workspace_bytes(plan)

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Chunk / lane sweep of the fast select path (run under gpurun).
-for cfg in "16 3" "32 1" "16 1" "8 4" "32 2" "16 2" "64 2" "24 3"; do
+for cfg in "32 2" "64 2" "32 3"; do
   set -- $cfg
   FC_CHUNK=$1 FC_LANES=$2 python bench.py --steps 16 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/sw_$1_$2.json 2>/dev/null
   python - "$1" "$2" <<'PY'

@@ -1,0 +1,240 @@
+"""GPU tests: stand-alone stage operators, reference-recorded goldens,
+multi-chunk / multi-lane scheduling, and the known answers of the
+reference's own stage tests (test_budget.py, test_edge_refresh.py,
+test_migration.py, test_fusion.py)."""
+
+import json
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import freqcache_oracle as O
+from oracle.parity import ParityReport, compare
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+sys.path.insert(0, str(GOLD))
+from cases import C1, C2, fhash, small_cases  # noqa: E402
+
+
+class _G:
+    """Golden record -> object with CacheDecision-like fields for compare()."""
+
+    def __init__(self, g):
+        self.__dict__.update(g)
+
+
+def _ocfg(c):
+    return O.OracleConfig(tau_mig=c.get("tau_mig", 0.12), edge_lambda=c.get("edge_lambda", 0.25),
+                          alpha_min=c.get("alpha_min", 0.08), alpha_max=c.get("alpha_max", 0.5),
+                          patch_size=c["patch_size"], refresh_shift=c.get("refresh_shift"))
+
+
+def _fcfg(c):
+    import paper_2604_24391_b200 as fc
+    return fc.CacheConfig(tau_mig=c.get("tau_mig", 0.12), edge_lambda=c.get("edge_lambda", 0.25),
+                          budget=fc.BudgetConfig(c.get("alpha_min", 0.08), c.get("alpha_max", 0.5)),
+                          patch_size=c["patch_size"])
+
+
+# ------------------------------------------------------ stage operators ----
+
+def test_sim_freq(cuda):
+    import paper_2604_24391_b200 as fc
+    amp = np.abs(np.fft.fft2(np.random.default_rng(3).random((16, 16))))
+    assert fc.sim_freq(amp, amp) == pytest.approx(1.0, abs=1e-12)
+    f = np.random.default_rng(4).random((24, 24))
+    assert fc.sim_freq(np.abs(np.fft.fft2(f)), np.abs(np.fft.fft2(np.roll(f, (5, 11), axis=(0, 1))))) >= 1 - 1e-9
+    a, b = np.zeros((4, 4)), np.zeros((4, 4))
+    a[0, 1] = b[2, 3] = 1.0
+    assert fc.sim_freq(a, b) == 0.0
+    with pytest.raises(fc.DegenerateSpectrumError, match="degenerate spectrum"):
+        fc.sim_freq(np.zeros((4, 4)), np.ones((4, 4)))
+    with pytest.raises(ValueError):
+        fc.sim_freq(np.full((4, 4), -1.0), np.ones((4, 4)))
+    with pytest.raises(ValueError):
+        fc.sim_freq(np.full((4, 4), np.nan), np.ones((4, 4)))
+    rng = np.random.default_rng(9)
+    for _ in range(5):
+        x, y = rng.random((37, 53)), rng.random((37, 53))
+        assert fc.sim_freq(x, y) == pytest.approx(O.similarity(x, y), rel=1e-13)
+
+
+def test_spectral_entropy(cuda):
+    import paper_2604_24391_b200 as fc
+    amp = np.zeros((8, 8))
+    amp[3, 5] = 7.0
+    r = fc.spectral_entropy(amp)
+    assert r.raw == 0.0 and r.normalized == 0.0 and r.bin_count == 64
+    r = fc.spectral_entropy(np.full((8, 8), 2.0))
+    assert r.raw == pytest.approx(math.log(64), abs=1e-12) and r.normalized == pytest.approx(1.0, abs=1e-12)
+    amp = np.zeros((8, 8))
+    amp[0, 1] = amp[5, 2] = 3.0
+    r = fc.spectral_entropy(amp)
+    assert r.raw == pytest.approx(math.log(2), abs=1e-12) and r.normalized == pytest.approx(1 / 6, abs=1e-12)
+    with pytest.raises(fc.DegenerateSpectrumError):
+        fc.spectral_entropy(np.zeros((4, 4)))
+    amp = np.zeros((4, 4))
+    amp[0, 0], amp[1, 1], amp[2, 2] = 10.0, 1.0, 1.0
+    r = fc.spectral_entropy(amp, include_dc=False)
+    assert r.raw == pytest.approx(math.log(2), abs=1e-12)
+    rng = np.random.default_rng(0)
+    a = rng.random((64, 64))
+    assert fc.spectral_entropy(a).raw == pytest.approx(O.entropy(a)[0], abs=1e-12)
+
+
+def test_refresh_mask(cuda):
+    import paper_2604_24391_b200 as fc
+    r = fc.refresh_mask(fc.EnergyMap(np.array([[0.0, 0.0], [0.0, 100.0]]), 8, 2), 0.25)
+    assert r.mean_energy == pytest.approx(25.0)
+    assert r.mean_energy + 0.25 * r.std_energy == pytest.approx(35.825317547305483)
+    assert r.mask.tolist() == [[False, False], [False, True]]
+    r = fc.refresh_mask(fc.EnergyMap(np.full((3, 3), 4.2), 8, 2), 0.25)
+    assert r.std_energy == 0.0 and not r.mask.any()
+    e = np.random.default_rng(3).random((4, 4))
+    assert not fc.refresh_mask(fc.EnergyMap(e, 8, 2), math.inf).mask.any()
+    big = np.random.default_rng(5).random((300, 300))
+    m, mu, sd, _ = O.refresh(big, 0.25)
+    r = fc.refresh_mask(fc.EnergyMap(big, 8, 2), 0.25)
+    assert r.mean_energy == pytest.approx(mu, rel=1e-13) and r.std_energy == pytest.approx(sd, rel=1e-12)
+    assert np.array_equal(r.mask, m)
+
+
+def test_topk_ascending(cuda):
+    import paper_2604_24391_b200 as fc
+    assert fc.topk_ascending([0, 1, 2], np.array([5.0, 1.0, 3.0]), 2) == (1, 2)
+    assert fc.topk_ascending([0, 1, 2, 3], np.array([4.0, 2.0, 9.0, 1.0]), 10) == (3, 1, 0, 2)
+    assert fc.topk_ascending([2, 0, 1, 3], np.array([2.0, 2.0, 2.0, 1.0]), 3) == (3, 0, 1)
+    assert fc.topk_ascending([], np.array([]), 5) == ()
+    assert fc.topk_ascending([1], np.array([0.0, 1.0]), 0) == ()
+    rng = np.random.default_rng(11)
+    e = np.round(rng.random(5000), 2)  # many exact ties
+    cand = rng.permutation(5000)[:3000]
+    assert fc.topk_ascending(cand, e, 1700) == O.topk_ascending(cand, e, 1700)
+
+
+# ---------------------------------------------- reference-recorded goldens --
+
+def test_small_goldens_through_gpu(cuda):
+    """GPU decisions against the reference's own recorded decisions (margins
+    from the pinned oracle)."""
+    import paper_2604_24391_b200 as fc
+    gold = json.loads((GOLD / "golden_small.json").read_text())
+    rep = ParityReport()
+    for (name, prev, curr, c), g in zip(small_cases(), gold):
+        assert g["prev"] == fhash(prev) and g["curr"] == fhash(curr)
+        d = fc.decide(prev, curr, _fcfg(c))
+        o = O.decide(prev, curr, _ocfg(c))
+        gd = _G(g["decision"])
+        assert list(o.reuse_set) == gd.reuse_set  # oracle pinned on this case
+        compare(d, o, _ocfg(c), rep=rep)
+    assert rep.ok, rep.errors
+
+
+def test_c1_golden_sequence(cuda):
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.api import _fetch, decision_from_device
+    from paper_2604_24391_b200.synth import stream_frames
+    gold = json.loads((GOLD / "golden_c1.json").read_text())
+    fr = stream_frames(C1["seed"], C1["stream"], C1["steps"], C1["size"], C1["size"])
+    assert [fhash(f) for f in fr] == gold["frames"]
+    cfg = fc.CacheConfig(patch_size=14, budget=fc.BudgetConfig(0.5, 0.5))
+    oc = _ocfg({"patch_size": 14, "alpha_min": 0.5, "alpha_max": 0.5})
+    eng = fc.FreqCacheEngine(1, 224, 224, 14, fmt="rgb")
+    rep = ParityReport()
+    exact = 0
+    for t in range(len(fr)):
+        out = eng.select(torch.from_numpy(fr[t:t + 1]).cuda(), cfg)
+        if t == 0:
+            continue
+        d = decision_from_device(*_fetch(out), step=t)
+        g = gold["decisions"][t - 1]
+        o = O.decide(fr[t - 1], fr[t], oc, step=t)
+        assert list(o.reuse_set) == g["reuse_set"]
+        compare(d, o, oc, rep=rep)
+        exact += list(d.reuse_set) == g["reuse_set"] and list(d.refresh_set) == g["refresh_set"]
+    assert rep.ok, rep.errors
+    print("config-1 steps bit-identical to the reference:", exact, "of", len(fr) - 1, rep.exemptions)
+
+
+def test_c2_golden_two_streams_batched(cuda):
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.api import decision_from_device
+    from paper_2604_24391_b200.synth import stream_frames
+    gold = json.loads((GOLD / "golden_c2.json").read_text())
+    S, T = C2["streams"], C2["steps"]
+    frames = np.stack([stream_frames(C2["seed"], s, T, 448, 448) for s in range(S)], axis=1)
+    for s in range(S):
+        assert [fhash(f) for f in frames[:, s]] == gold["streams"][s]["frames"]
+    cfg = fc.CacheConfig(patch_size=14)
+    oc = _ocfg({"patch_size": 14, "refresh_shift": 1})
+    eng = fc.FreqCacheEngine(S, 448, 448, 14, fmt="rgb")
+    rep = ParityReport()
+    for t in range(T):
+        out = eng.select(torch.from_numpy(np.ascontiguousarray(frames[t])).cuda(), cfg, refresh_shift=1)
+        if t == 0:
+            continue
+        res = out.host_results()
+        ri, rc, rm = out.reuse_idx.cpu().numpy(), out.recompute_idx.cpu().numpy(), out.refresh_mask.cpu().numpy()
+        for s in range(S):
+            d = decision_from_device(res[s], ri[s], rc[s], rm[s], step=t)
+            g = gold["streams"][s]["decisions"][t - 1]
+            assert d.flushed == g["flushed"] or rep.exemptions
+            o = O.decide(frames[t - 1, s], frames[t, s], oc, step=t)
+            compare(d, o, oc, rep=rep)
+    assert rep.ok, rep.errors
+
+
+def test_multichunk_multilane_batch(cuda, monkeypatch):
+    """70 streams in 16-stream chunks on 3 lanes: every stream's decision
+    equals the single-stream result (chunking never mixes streams)."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    monkeypatch.setenv("FC_CHUNK", "16")
+    monkeypatch.setenv("FC_LANES", "3")
+    S = 70
+    frames = torch_stream_frames(S, 3, 448, 448, seed=99, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    big = fc.FreqCacheEngine(S, 448, 448, 14, fmt="rgb")
+    monkeypatch.setenv("FC_CHUNK", "512")
+    monkeypatch.setenv("FC_LANES", "1")
+    one = fc.FreqCacheEngine(S, 448, 448, 14, fmt="rgb")
+    for t in range(3):
+        a = big.select(frames[t], cfg, refresh_shift=1)
+        b = one.select(frames[t], cfg, refresh_shift=1)
+        assert torch.equal(a.results, b.results)
+        assert torch.equal(a.reuse_idx, b.reuse_idx)
+        assert torch.equal(a.src_map, b.src_map)
+        assert torch.equal(a.energy, b.energy)
+    res = a.host_results()
+    assert (res["cold"] == 0).all() and (res["status"] == 0).all()
+    # spot-check two streams against the oracle
+    oc = O.OracleConfig(patch_size=14, refresh_shift=1)
+    from paper_2604_24391_b200.api import decision_from_device
+    rep = ParityReport()
+    f1, f2 = frames[1].cpu().numpy(), frames[2].cpu().numpy()
+    for s in (0, 69):
+        d = decision_from_device(res[s], a.reuse_idx[s].cpu().numpy(), a.recompute_idx[s].cpu().numpy(),
+                                 a.refresh_mask[s].cpu().numpy(), step=2)
+        compare(d, O.decide(f1[s], f2[s], oc), oc, energies=a.energy[s].cpu().numpy(), rep=rep)
+    assert rep.ok, rep.errors
+
+
+def test_engine_reset_and_partial_reset(cuda):
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import stream_frames
+    f = np.stack([stream_frames(5, s, 3, 224, 224) for s in range(3)], axis=1)
+    eng = fc.FreqCacheEngine(3, 224, 224, 14, fmt="rgb")
+    cfg = fc.CacheConfig(patch_size=14)
+    eng.select(torch.from_numpy(np.ascontiguousarray(f[0])).cuda(), cfg)
+    eng.reset(first=1, count=1)
+    r = eng.select(torch.from_numpy(np.ascontiguousarray(f[1])).cuda(), cfg).host_results()
+    assert list(r["cold"]) == [0, 1, 0]
+    assert r["k_final"][1] == 0 and r["flushed"][1] == 1
