@@ -297,7 +297,8 @@ __global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, co
 // One CTA per (kBC-column block, stream); 64*kBC threads, column c = t % kBC
 // fastest.  The T1 block and the stream's previous spectrum are staged by
 // two TMA bulk copies at kernel start.  State layout is the register order
-// of the forward column FFT: spec[b][cb][t][j2] (64 B per thread).
+// of the forward column FFT: spec[b][cb][i][t] float4 (j2 = 2i, 2i+1), so
+// the state swap is coalesced and its shared-memory reads conflict-free.
 constexpr int kT1Block = 448 * kBC * 8;      // bytes
 constexpr int kStBlock = 64 * kBC * 8 * 8;   // bytes
 constexpr int kXCB = 516;                    // scratch stride, 4 interleaved transforms
@@ -336,21 +337,21 @@ __global__ void __launch_bounds__(64 * kBC, 4) k448_cols(KParams kp, int b0) {
 
   const bool act = r < 56;
   const int k1 = r >> 3, j1 = r & 7;
-  float4* st = reinterpret_cast<float4*>(stg + (size_t)t * 8);
+  float4* st = reinterpret_cast<float4*>(stg) + t;  // chunk i at st[i * 64 * kBC]
   // the previous spectrum must have landed before this block is overwritten
   if (valid) tma::bar_wait(&bar[1], 0);
   __syncthreads();
   if (act) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) st[i] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
+    for (int i = 0; i < 4; ++i) st[i * 64 * kBC] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
   }
   if (!valid) return;  // cold stream: spectrum established (block-uniform)
   float2 p[8];
   if (act) {
-    const float4* pv = reinterpret_cast<const float4*>(prev + (size_t)t * 8);
+    const float4* pv = reinterpret_cast<const float4*>(prev) + t;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float4 q = pv[i];
+      const float4 q = pv[i * 64 * kBC];
       p[2 * i] = make_float2(q.x, q.y);
       p[2 * i + 1] = make_float2(q.z, q.w);
     }
@@ -581,18 +582,18 @@ __global__ void __launch_bounds__(64 * kBC, 3) k448_cols_p(KParams kp, int b0, i
     f448::fwd<false>(a, v, S, r, tw);
     const bool act = r < 56;
     const int k1 = r >> 3, j1 = r & 7;
-    float4* st = reinterpret_cast<float4*>(stg + (size_t)t * 8);
+    float4* st = reinterpret_cast<float4*>(stg) + t;  // chunk i at st[i * 64 * kBC]
     if (act) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) st[i] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
+      for (int i = 0; i < 4; ++i) st[i * 64 * kBC] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
     }
     if (valid) {
       float2 p[8];
       if (act) {
-        const float4* pv = reinterpret_cast<const float4*>(prev + (size_t)t * 8);
+        const float4* pv = reinterpret_cast<const float4*>(prev) + t;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float4 q = pv[i];
+          const float4 q = pv[i * 64 * kBC];
           p[2 * i] = make_float2(q.x, q.y);
           p[2 * i + 1] = make_float2(q.z, q.w);
         }
