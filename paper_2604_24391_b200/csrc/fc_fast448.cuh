@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, co
   unsigned char* px = smem;                                          // stripe pixels
   float2* zin = reinterpret_cast<float2*>(smem + kPxBytes448);       // [7][448]
   float2* S = reinterpret_cast<float2*>(smem);                       // [7][504] (after phase 1)
-  double* part = reinterpret_cast<double*>(smem + 7 * f448::XR * 8); // [4][448]
-  double* ysq = part + 4 * 448;                                      // [288]
+  double* part = reinterpret_cast<double*>(smem + 7 * f448::XR * 8); // [4][32 x 15]
+  double* ysq = part + 4 * 480;                                      // [9][32]
 
   // ---- phase 0: stage the stripe with the TMA engine
   const size_t row0 = ((size_t)b * 448 + (size_t)s * 14) * 448;
@@ -221,10 +221,16 @@ __global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, co
   }
   const int anyvary = __syncthreads_or(vary);  // also: pixels consumed
   const int anybad = __syncthreads_or(emax == 0x7ff00000u);
-  part[0 * 448 + t] = tu0;
-  part[1 * 448 + t] = tu1;
-  part[2 * 448 + t] = tu2;
-  part[3 * 448 + t] = s2;
+  // per-patch stride 15 (one pad double): phase-2 reads of 32 patches hit
+  // 16 distinct bank pairs per half-warp
+  {
+    const int pp = t / 14, y = t - (t / 14) * 14;
+    double* pc = part + pp * 15 + y;
+    pc[0 * 480] = tu0;
+    pc[1 * 480] = tu1;
+    pc[2 * 480] = tu2;
+    pc[3 * 480] = s2;
+  }
   if (t == 0) {
     StripeStat st;
     st.ref = ref; st.unused = 0.0; st.nonfinite = anybad; st.varying = anyvary;
@@ -232,10 +238,10 @@ __global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, co
     kp.stripes[(size_t)b * 32 + s] = st;
   }
   __syncthreads();
-  // ---- phase 2: low-frequency corner per patch (fp64)
+  // ---- phase 2: low-frequency corner per patch (fp64); warp = (u, v), lane = patch
   if (t < 288) {
-    const int pp = t / 9, uv = t - (t / 9) * 9, u = uv / 3, v = uv - (uv / 3) * 3;
-    const double* tp = part + u * 448 + pp * 14;
+    const int uv = t >> 5, pp = t & 31, u = uv / 3, v = uv - (uv / 3) * 3;
+    const double* tp = part + u * 480 + pp * 15;
     double y = 0.0;
 #pragma unroll
     for (int q = 0; q < 14; ++q) y = fma(tp[q], dc.c[v][q], y);
@@ -243,13 +249,13 @@ __global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, co
   }
   __syncthreads();
   if (t < 32) {
-    const double* sp = part + 3 * 448 + t * 14;
+    const double* sp = part + 3 * 480 + t * 15;
     double e = 0.0;
 #pragma unroll
     for (int q = 0; q < 14; ++q) e += sp[q];
     double low = 0.0;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) low += ysq[t * 9 + q];
+    for (int q = 0; q < 9; ++q) low += ysq[q * 32 + t];
     e -= low;
     kp.energy[(size_t)b * 1024 + s * 32 + t] = e > 0.0 ? e : 0.0;
   }
