@@ -158,6 +158,12 @@ int  fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                int32_t fresh_layout, void* out, int64_t* out_ages,
                void* cuda_stream);
 
+/* Decision mask images (frameio.py:188-219): img[b][p] = 255 reused, 128
+ * edge-forced recompute, 0 otherwise; flushed or cold streams all 0.        */
+int  fc_render_masks(int32_t batch, int32_t n_tokens, const fc_stream_result* results,
+                     const uint8_t* reuse_mask, const uint8_t* refresh_mask,
+                     uint8_t* img, void* cuda_stream);
+
 /* ---- stand-alone stage operators on arbitrary fp64 arrays (device pointers).
  * `ws` is a device scratch buffer of fc_stage_workspace_bytes(); results are
  * written to device memory; `flags` (device int32): bit0 non-finite input,

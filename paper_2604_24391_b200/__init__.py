@@ -53,3 +53,4 @@ from .api import (  # noqa: F401
     topk_ascending,
 )
 from .engine import FreqCacheEngine, SelectResult, splice, splice_map  # noqa: F401
+from . import records  # noqa: F401

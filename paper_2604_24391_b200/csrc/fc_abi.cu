@@ -525,6 +525,32 @@ int fc_splice_map(int32_t rows, int32_t cols, const int32_t* reuse_idx, int32_t 
   return launch_check();
 }
 
+// --------------------------------------------------------- mask images ----
+
+namespace {
+__global__ void k_render_masks(int B, int N, const fc_stream_result* __restrict__ res,
+                               const uint8_t* __restrict__ reuse, const uint8_t* __restrict__ fresh,
+                               uint8_t* __restrict__ img) {
+  // frameio.py:188-219: reused 255, edge-forced recompute 128, other 0;
+  // flushed (and cold) steps render all-zero
+  const int64_t total = (int64_t)B * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / N);
+    const bool fl = res[b].flushed != 0;
+    img[i] = fl ? 0 : (reuse[i] ? 255 : (fresh[i] ? 128 : 0));
+  }
+}
+}  // namespace
+
+int fc_render_masks(int32_t batch, int32_t n_tokens, const fc_stream_result* results, const uint8_t* reuse_mask,
+                    const uint8_t* refresh_mask, uint8_t* img, void* stream) {
+  if (batch < 1 || n_tokens < 1 || !results || !reuse_mask || !refresh_mask || !img) return FC_EINVAL;
+  const int64_t total = (int64_t)batch * n_tokens;
+  const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  k_render_masks<<<blocks, 256, 0, as_stream(stream)>>>(batch, n_tokens, results, reuse_mask, refresh_mask, img);
+  return launch_check();
+}
+
 // ---------------------------------------------------------- stage ops ----
 
 static int stage_blocks(int64_t n) {

@@ -238,3 +238,43 @@ def test_engine_reset_and_partial_reset(cuda):
     r = eng.select(torch.from_numpy(np.ascontiguousarray(f[1])).cuda(), cfg).host_results()
     assert list(r["cold"]) == [0, 1, 0]
     assert r["k_final"][1] == 0 and r["flushed"][1] == 1
+
+
+def test_records_rerun_byte_identical(cuda, tmp_path):
+    """Acceptance criterion 7 of the reference (test_acceptance.py:207-234):
+    identical inputs give byte-identical JSONL / CSV / PGM outputs; masks
+    rendered on the GPU equal the index-set rendering."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200 import records
+    rng = np.random.default_rng(21)
+    base = rng.random((64, 64))
+    frames = [np.roll(base, (3 * t, 5 * t), axis=(0, 1)) for t in range(8)]
+    cfg = fc.CacheConfig(patch_size=8)
+    outs = []
+    for run in ("a", "b"):
+        rep = fc.run_sequence(frames, cfg)
+        d = tmp_path / run
+        d.mkdir()
+        records.write_decisions_jsonl(d / "decisions.jsonl", rep.decisions)
+        records.write_metrics_csv(d / "metrics.csv", rep)
+        records.export_masks(records.read_decisions_jsonl(d / "decisions.jsonl"), d / "masks")
+        outs.append(d)
+    for name in ("decisions.jsonl", "metrics.csv"):
+        assert (outs[0] / name).read_bytes() == (outs[1] / name).read_bytes()
+    pa, pb = sorted((outs[0] / "masks").glob("*.pgm")), sorted((outs[1] / "masks").glob("*.pgm"))
+    assert len(pa) == 7 and all(x.read_bytes() == y.read_bytes() for x, y in zip(pa, pb))
+    # device-rendered masks == host rendering of the same decisions
+    eng = fc.FreqCacheEngine(1, 64, 64, 8, fmt="gray64")
+    dev_imgs, decs = [], []
+    from paper_2604_24391_b200.api import _fetch, decision_from_device
+    for t, f in enumerate(frames):
+        out = eng.select(torch.from_numpy(f).cuda().unsqueeze(0), cfg)
+        if t == 0:
+            continue
+        dev_imgs.append(records.render_masks(out, eng)[0].cpu().numpy())
+        decs.append(decision_from_device(*_fetch(out), step=t))
+    paths = records.export_masks(decs, tmp_path / "host")
+    for img, p in zip(dev_imgs, paths):
+        data = p.read_bytes()
+        assert data.endswith(img.tobytes())
