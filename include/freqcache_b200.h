@@ -151,12 +151,14 @@ int  fc_patch_energy(const fc_plan* plan, const void* frames, void* workspace,
 
 /* Splice: out[b][p] = src_map[b][p] >= 0 ? cache[b][src] : fresh[b][...];
  * out_ages likewise (cache_ages+1 / 0).  cache may be NULL when every entry
- * of src_map is negative.  row_bytes = D * element size (any, bit copy). */
+ * of src_map is negative.  row_bytes = D * element size (any, bit copy).
+ * fresh_rows: rows per stream in `fresh` (ignored for FC_FRESH_DENSE, where
+ * it is n_tokens; for FC_FRESH_COMPACT any capacity >= the recompute count). */
 int  fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                const int32_t* src_map, const void* cache,
                const int64_t* cache_ages, const void* fresh,
-               int32_t fresh_layout, void* out, int64_t* out_ages,
-               void* cuda_stream);
+               int32_t fresh_layout, int32_t fresh_rows, void* out,
+               int64_t* out_ages, void* cuda_stream);
 
 /* Decision mask images (frameio.py:188-219): img[b][p] = 255 reused, 128
  * edge-forced recompute, 0 otherwise; flushed or cold streams all 0.        */

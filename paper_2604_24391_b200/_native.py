@@ -109,7 +109,7 @@ def load(path=None):
         "fc_select_profile": (C.c_int, [vp, C.POINTER(Config), vp, vp, vp, C.POINTER(SelectOut),
                                         C.POINTER(C.c_float), vp]),
         "fc_patch_energy": (C.c_int, [vp, vp, vp, vp, vp]),
-        "fc_splice": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, i32, vp, vp, vp]),
+        "fc_splice": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
         "fc_splice_map": (C.c_int, [i32, i32, vp, i32, i32, i32, vp, vp, vp]),
         "fc_stage_workspace_bytes": (i64, []),
         "fc_render_masks": (C.c_int, [i32, i32, vp, vp, vp, vp, vp]),

@@ -479,10 +479,12 @@ int fc_patch_energy(const fc_plan* pl, const void* frames, void* ws, double* ene
 }
 
 int fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, const void* cache,
-              const int64_t* cache_ages, const void* fresh, int32_t fresh_layout, void* out,
+              const int64_t* cache_ages, const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* out,
               int64_t* out_ages, void* stream) {
   if (batch < 1 || n_tokens < 1 || row_bytes < 1 || !src_map || !fresh || !out || !out_ages) return FC_EINVAL;
   if (fresh_layout != FC_FRESH_DENSE && fresh_layout != FC_FRESH_COMPACT) return FC_EINVAL;
+  if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
+  if (fresh_rows < 1) return FC_EINVAL;
   const int total = batch * n_tokens;
   const int compact = fresh_layout == FC_FRESH_COMPACT;
   const cudaStream_t st = as_stream(stream);
@@ -500,11 +502,11 @@ int fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t*
     if (blocks > cap) blocks = cap;
     k_splice16<UNR><<<blocks, FC_THREADS, 0, st>>>(
         total, n_tokens, row_bytes / 16, src_map, reinterpret_cast<const int4*>(cache), cache_ages,
-        reinterpret_cast<const int4*>(fresh), compact, reinterpret_cast<int4*>(out), out_ages);
+        reinterpret_cast<const int4*>(fresh), compact, fresh_rows, reinterpret_cast<int4*>(out), out_ages);
   } else {
     k_splice_bytes<<<total, 128, 0, st>>>(total, n_tokens, row_bytes, src_map,
                                           reinterpret_cast<const uint8_t*>(cache), cache_ages,
-                                          reinterpret_cast<const uint8_t*>(fresh), compact,
+                                          reinterpret_cast<const uint8_t*>(fresh), compact, fresh_rows,
                                           reinterpret_cast<uint8_t*>(out), out_ages);
   }
   return launch_check();

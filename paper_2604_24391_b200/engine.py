@@ -67,7 +67,9 @@ class FreqCacheEngine:
         if fmt not in _FORMATS:
             raise ValueError(f"unknown frame format {fmt!r}")
         self.lib = nat.lib()
-        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.fmt = fmt
         self.format_code, self.dtype, self.channels = _FORMATS[fmt]
         self.batch, self.height, self.width, self.patch_size = int(batch), int(height), int(width), int(patch_size)
@@ -184,9 +186,11 @@ def splice(src_map, cache, cache_ages, fresh, out, out_ages, compact=False):
         raise ValueError("cache and out must share dtype and shape")
     if fresh.dtype != out.dtype or fresh.shape[-1] != out.shape[-1]:
         raise ValueError("fresh rows must match out's dtype and row width")
+    if fresh.dim() != 3 or fresh.shape[0] != B or (not compact and fresh.shape[1] != N):
+        raise ValueError("fresh must be [B, N, D] (dense) or [B, K, D] (compact)")
     rc = lib.fc_splice(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(cache),
                        _ptr(cache_ages), _ptr(fresh),
-                       nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE,
+                       nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE, int(fresh.shape[1]),
                        _ptr(out), _ptr(out_ages), _stream(out.device))
     nat.check(rc, "fc_splice")
     return out, out_ages

@@ -278,3 +278,33 @@ def test_records_rerun_byte_identical(cuda, tmp_path):
     for img, p in zip(dev_imgs, paths):
         data = p.read_bytes()
         assert data.endswith(img.tobytes())
+
+
+def test_vit_cached_encoder_small(cuda):
+    """Config-4 plumbing on a small ViT: cold steps equal a full recompute;
+    reused rows are bit copies of the shifted cache."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    from paper_2604_24391_b200.vit import CachedEncoder, ViT, ViTConfig, cosine
+    c = ViTConfig(image=112, patch=14, width=64, mlp=128, heads=2, layers=3)
+    model = ViT(c).cuda().float().eval()
+    frames = torch_stream_frames(2, 4, 112, 112, seed=3, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    with torch.no_grad():
+        for mode in ("layer1", "subset"):
+            enc = CachedEncoder(model, 2, mode=mode)
+            y0, out0 = enc.step(frames[0], cfg)
+            assert (out0.host_results()["cold"] == 1).all()
+            ref = model(frames[0])
+            assert torch.allclose(y0, ref, atol=2e-5, rtol=1e-4)
+            prev_h = enc.h1[enc.cur].clone()
+            y1, out1 = enc.step(frames[1], cfg)
+            cache_now = enc.h1[enc.cur]
+            sm = out1.src_map
+            for b in range(2):
+                for p in range(c.tokens):
+                    s = int(sm[b, p])
+                    if s >= 0:
+                        assert torch.equal(cache_now[b, p], prev_h[b, s])
+            assert float(cosine(y1, model(frames[1])).min()) > 0.5
