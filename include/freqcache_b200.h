@@ -188,6 +188,15 @@ int  fc_topk_ascending(const int64_t* cand, int64_t m, const double* energies,
                        int64_t n_energies, int64_t k, int64_t* out,
                        int32_t* flags, void* cuda_stream);
 
+/* fc_splice with ragged fresh rows: stream b's k-th recomputed token (row-
+ * major) is row fresh_offsets[b] + k of `fresh` (device int64 [B]), e.g. the
+ * packed values of a variable-length encoder batch. */
+int  fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes,
+                      const int32_t* src_map, const void* cache,
+                      const int64_t* cache_ages, const void* fresh,
+                      const int64_t* fresh_offsets, void* out, int64_t* out_ages,
+                      void* cuda_stream);
+
 /* Build src_map for one stream from an ordered reuse list (fusion.py:481-504).
  * flag (device int32, may be NULL) receives FC_EBOUNDS on an out-of-bounds
  * source. */

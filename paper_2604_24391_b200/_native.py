@@ -42,7 +42,7 @@ EXPORTS = (
     "fc_plan_state_bytes", "fc_plan_workspace_bytes", "fc_plan_tokens",
     "fc_state_reset", "fc_select", "fc_select_profile", "fc_patch_energy", "fc_splice",
     "fc_splice_map", "fc_stage_workspace_bytes", "fc_amp_cosine", "fc_spectral_sums",
-    "fc_refresh_mask", "fc_topk_ascending", "fc_render_masks",
+    "fc_refresh_mask", "fc_topk_ascending", "fc_render_masks", "fc_splice_packed",
 )
 
 
@@ -113,6 +113,7 @@ def load(path=None):
         "fc_splice_map": (C.c_int, [i32, i32, vp, i32, i32, i32, vp, vp, vp]),
         "fc_stage_workspace_bytes": (i64, []),
         "fc_render_masks": (C.c_int, [i32, i32, vp, vp, vp, vp, vp]),
+        "fc_splice_packed": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
         "fc_amp_cosine": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
         "fc_spectral_sums": (C.c_int, [vp, i64, i32, vp, vp, vp, vp]),
         "fc_refresh_mask": (C.c_int, [vp, i64, C.c_double, vp, vp, vp, vp]),

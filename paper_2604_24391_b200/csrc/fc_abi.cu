@@ -478,16 +478,11 @@ int fc_patch_energy(const fc_plan* pl, const void* frames, void* ws, double* ene
   return launch_check();
 }
 
-int fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, const void* cache,
-              const int64_t* cache_ages, const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* out,
-              int64_t* out_ages, void* stream) {
-  if (batch < 1 || n_tokens < 1 || row_bytes < 1 || !src_map || !fresh || !out || !out_ages) return FC_EINVAL;
-  if (fresh_layout != FC_FRESH_DENSE && fresh_layout != FC_FRESH_COMPACT) return FC_EINVAL;
-  if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
-  if (fresh_rows < 1) return FC_EINVAL;
+static int splice_impl(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map,
+                       const void* cache, const int64_t* cache_ages, const void* fresh, int compact,
+                       int32_t fresh_rows, const int64_t* fresh_off, void* out, int64_t* out_ages,
+                       cudaStream_t st) {
   const int total = batch * n_tokens;
-  const int compact = fresh_layout == FC_FRESH_COMPACT;
-  const cudaStream_t st = as_stream(stream);
   const bool vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(cache) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(fresh) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
@@ -502,14 +497,35 @@ int fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t*
     if (blocks > cap) blocks = cap;
     k_splice16<UNR><<<blocks, FC_THREADS, 0, st>>>(
         total, n_tokens, row_bytes / 16, src_map, reinterpret_cast<const int4*>(cache), cache_ages,
-        reinterpret_cast<const int4*>(fresh), compact, fresh_rows, reinterpret_cast<int4*>(out), out_ages);
+        reinterpret_cast<const int4*>(fresh), compact, fresh_rows, fresh_off, reinterpret_cast<int4*>(out),
+        out_ages);
   } else {
     k_splice_bytes<<<total, 128, 0, st>>>(total, n_tokens, row_bytes, src_map,
                                           reinterpret_cast<const uint8_t*>(cache), cache_ages,
-                                          reinterpret_cast<const uint8_t*>(fresh), compact, fresh_rows,
+                                          reinterpret_cast<const uint8_t*>(fresh), compact, fresh_rows, fresh_off,
                                           reinterpret_cast<uint8_t*>(out), out_ages);
   }
   return launch_check();
+}
+
+int fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, const void* cache,
+              const int64_t* cache_ages, const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* out,
+              int64_t* out_ages, void* stream) {
+  if (batch < 1 || n_tokens < 1 || row_bytes < 1 || !src_map || !fresh || !out || !out_ages) return FC_EINVAL;
+  if (fresh_layout != FC_FRESH_DENSE && fresh_layout != FC_FRESH_COMPACT) return FC_EINVAL;
+  if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
+  if (fresh_rows < 1) return FC_EINVAL;
+  return splice_impl(batch, n_tokens, row_bytes, src_map, cache, cache_ages, fresh,
+                     fresh_layout == FC_FRESH_COMPACT, fresh_rows, nullptr, out, out_ages, as_stream(stream));
+}
+
+int fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map,
+                     const void* cache, const int64_t* cache_ages, const void* fresh,
+                     const int64_t* fresh_offsets, void* out, int64_t* out_ages, void* stream) {
+  if (batch < 1 || n_tokens < 1 || row_bytes < 1 || !src_map || !fresh || !fresh_offsets || !out || !out_ages)
+    return FC_EINVAL;
+  return splice_impl(batch, n_tokens, row_bytes, src_map, cache, cache_ages, fresh, 1, 0, fresh_offsets, out,
+                     out_ages, as_stream(stream));
 }
 
 int fc_splice_map(int32_t rows, int32_t cols, const int32_t* reuse_idx, int32_t k, int32_t dip, int32_t djp,

@@ -830,7 +830,8 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice16(int total, int n_tokens
                                                          const int4* __restrict__ cache,
                                                          const int64_t* __restrict__ cache_ages,
                                                          const int4* __restrict__ fresh, int compact,
-                                                         int fresh_rows, int4* __restrict__ out,
+                                                         int fresh_rows, const int64_t* __restrict__ fresh_off,
+                                                         int4* __restrict__ out,
                                                          int64_t* __restrict__ out_ages) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -848,7 +849,10 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice16(int total, int n_tokens
       const int s = src_map[rr];
       const size_t base = (size_t)bs * n_tokens;
       if (s >= 0) src[u] = cache + (base + s) * row16;
-      else src[u] = fresh + ((size_t)bs * fresh_rows + (compact ? (-s - 1) : (rr - bs * n_tokens))) * row16;
+      else {
+        const size_t row0 = fresh_off ? (size_t)fresh_off[bs] : (size_t)bs * fresh_rows;
+        src[u] = fresh + (row0 + (compact ? (-s - 1) : (rr - bs * n_tokens))) * row16;
+      }
       dst[u] = out + (size_t)rr * row16;
       if (on[u] && lane == 0)
         out_ages[rr] = s >= 0 ? cache_ages[base + s] + 1 : 0;
@@ -877,14 +881,16 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice16(int total, int n_tokens
 __global__ void k_splice_bytes(int total, int n_tokens, int64_t row_bytes, const int32_t* __restrict__ src_map,
                                const uint8_t* __restrict__ cache, const int64_t* __restrict__ cache_ages,
                                const uint8_t* __restrict__ fresh, int compact, int fresh_rows,
-                               uint8_t* __restrict__ out, int64_t* __restrict__ out_ages) {
+                               const int64_t* __restrict__ fresh_off, uint8_t* __restrict__ out,
+                               int64_t* __restrict__ out_ages) {
   const int row = blockIdx.x;
   if (row >= total) return;
   const int bs = row / n_tokens;
   const int s = src_map[row];
   const size_t base = (size_t)bs * n_tokens;
   const uint8_t* src = s >= 0 ? cache + (base + s) * row_bytes
-                              : fresh + ((size_t)bs * fresh_rows + (compact ? (-s - 1) : (row - bs * n_tokens))) * row_bytes;
+                              : fresh + ((fresh_off ? (size_t)fresh_off[bs] : (size_t)bs * fresh_rows) +
+                                         (compact ? (-s - 1) : (row - bs * n_tokens))) * row_bytes;
   for (int64_t c = threadIdx.x; c < row_bytes; c += blockDim.x) out[(size_t)row * row_bytes + c] = src[c];
   if (threadIdx.x == 0) out_ages[row] = s >= 0 ? cache_ages[base + s] + 1 : 0;
 }

@@ -196,6 +196,23 @@ def splice(src_map, cache, cache_ages, fresh, out, out_ages, compact=False):
     return out, out_ages
 
 
+def splice_packed(src_map, cache, cache_ages, fresh_values, fresh_offsets, out, out_ages):
+    """Splice with ragged fresh rows: stream b's k-th recomputed token is
+    ``fresh_values[fresh_offsets[b] + k]`` ([total, D]; offsets int64 [B])."""
+    lib = nat.lib()
+    B, N = src_map.shape
+    row_bytes = out.shape[-1] * out.element_size()
+    if fresh_values.dim() != 2 or fresh_values.shape[-1] != out.shape[-1] or fresh_values.dtype != out.dtype:
+        raise ValueError("fresh_values must be [total, D] with out's dtype")
+    if fresh_offsets.dtype != torch.int64 or fresh_offsets.numel() < B:
+        raise ValueError("fresh_offsets must be int64 [B]")
+    rc = lib.fc_splice_packed(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(cache), _ptr(cache_ages),
+                              _ptr(fresh_values), _ptr(fresh_offsets), _ptr(out), _ptr(out_ages),
+                              _stream(out.device))
+    nat.check(rc, "fc_splice_packed")
+    return out, out_ages
+
+
 def splice_map(rows, cols, reuse_idx, di_patches, dj_patches, src_map=None, flag=None):
     """Device src_map for one stream from an ordered reuse list."""
     lib = nat.lib()

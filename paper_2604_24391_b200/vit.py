@@ -34,7 +34,7 @@ from dataclasses import dataclass
 import torch
 import torch.nn.functional as F
 
-from .engine import FreqCacheEngine, splice
+from .engine import FreqCacheEngine, splice, splice_packed
 
 
 @dataclass(frozen=True)
@@ -63,8 +63,8 @@ class Block(torch.nn.Module):
         self.fc2 = torch.nn.Linear(c.mlp, c.width)
 
     def _heads(self, x):
-        b, n, d = x.shape
-        return x.view(b, n, self.h, d // self.h).transpose(1, 2)
+        # works for dense [B, n, D] and jagged nested [B, j, D] tensors
+        return x.unflatten(-1, (self.h, x.shape[-1] // self.h)).transpose(1, 2)
 
     def attn(self, xq, xkv, key_padding=None):
         """Attention with queries from xq and keys/values from xkv."""
@@ -76,7 +76,7 @@ class Block(torch.nn.Module):
         v = self._heads(F.linear(xkv, wv, bv))
         mask = None if key_padding is None else key_padding[:, None, None, :]
         o = F.scaled_dot_product_attention(q, k, v, attn_mask=mask)
-        return self.proj(o.transpose(1, 2).reshape(xq.shape))
+        return self.proj(o.transpose(1, 2).flatten(-2))
 
     def forward(self, x, key_padding=None):
         y = self.ln1(x)
@@ -131,11 +131,11 @@ def _gather_rows(x, idx):
 class CachedEncoder:
     """Batched token-cache encoder over B streams (select + partial ViT + splice)."""
 
-    def __init__(self, model: ViT, batch: int, mode: str = "layer1", device="cuda"):
+    def __init__(self, model: ViT, batch: int, mode: str = "layer1", device="cuda", group: int = 0):
         if mode not in ("layer1", "subset"):
             raise ValueError(mode)
         c = model.c
-        self.m, self.mode, self.B = model, mode, batch
+        self.m, self.mode, self.B, self.group = model, mode, batch, (group or batch)
         self.engine = FreqCacheEngine(batch, c.image, c.image, c.patch, fmt="rgb", device=device)
         n, d = c.tokens, c.width
         dt = next(model.parameters()).dtype
@@ -172,12 +172,29 @@ class CachedEncoder:
                 x = blk(x)
             y = m.ln(x)
         else:
-            x = x0
-            for blk in m.blocks:
-                x = blk(x, key_padding=valid)
-            y_rec = m.ln(x)
-            splice(out.src_map, self.h1[i], self.ages[i], y_rec.contiguous(), self.h1[o], self.ages[o],
-                   compact=True)
+            # streams sorted by recompute count and run in groups, each padded
+            # only to its own (128-bucketed) maximum; outputs are packed in
+            # stream order and spliced with per-stream offsets
+            counts = valid.sum(dim=1)
+            offsets = torch.zeros(B + 1, dtype=torch.int64, device=rec.device)
+            offsets[1:] = torch.cumsum(counts, 0)
+            total = int(offsets[-1].item())
+            packed = torch.empty((max(total, 1), x0.shape[-1]), dtype=x0.dtype, device=x0.device)
+            cnt = counts.tolist()
+            order = sorted(range(B), key=lambda b: cnt[b])
+            for g0 in range(0, B, self.group):
+                grp = order[g0:g0 + self.group]
+                kg = min(rec.shape[1], max(128, -(-max(cnt[b] for b in grp) // 128) * 128))
+                gi = torch.tensor(grp, device=rec.device)
+                vg = valid[gi, :kg]
+                x = x0[gi, :kg]
+                for blk in m.blocks:
+                    x = blk(x, key_padding=vg)
+                yg = m.ln(x)
+                pos = offsets[gi][:, None] + torch.arange(kg, device=rec.device)[None, :]
+                packed[pos[vg]] = yg[vg]
+            splice_packed(out.src_map, self.h1[i], self.ages[i], packed, offsets[:B].contiguous(),
+                          self.h1[o], self.ages[o])
             y = self.h1[o]
         self.cur = o
         return y, out
