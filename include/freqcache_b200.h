@@ -197,6 +197,18 @@ int  fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                       const int64_t* fresh_offsets, void* out, int64_t* out_ages,
                       void* cuda_stream);
 
+/* In-place splice over a per-stream ping-pong pair of caches.  slot_in[b]
+ * (device u8) names the buffer (0/1) holding stream b's cache.  A stream whose
+ * reused tokens all keep their slot (zero displacement) is updated in place:
+ * reused rows are not touched (age + 1) and only recomputed rows are written.
+ * Any other stream is spliced into its other buffer.  slot_out[b] receives the
+ * buffer now holding the result.  Rows must be 16-byte multiples/aligned.   */
+int  fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes,
+                       const int32_t* src_map, void* cache0, void* cache1,
+                       int64_t* ages0, int64_t* ages1, const uint8_t* slot_in,
+                       uint8_t* slot_out, const void* fresh, int32_t fresh_layout,
+                       int32_t fresh_rows, void* cuda_stream);
+
 /* Build src_map for one stream from an ordered reuse list (fusion.py:481-504).
  * flag (device int32, may be NULL) receives FC_EBOUNDS on an out-of-bounds
  * source. */

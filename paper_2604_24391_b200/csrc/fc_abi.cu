@@ -290,7 +290,7 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     const int nchunks = (int)((B + pl->chunk - 1) / pl->chunk);
     pl->lanes = env_int("FC_LANES", kLanesDefault, 1, kMaxLanes);
     if (pl->lanes > nchunks) pl->lanes = nchunks;
-    pl->smemA = (size_t)kPxBytes448 + (size_t)7 * 448 * sizeof(float2);
+    pl->smemA = (size_t)kPxBytes448;
     pl->smemB = (size_t)kScratchB + kStBlock + (size_t)2 * 448 * sizeof(float2);
     pl->smemC = (size_t)(kBP * f448::XR) * sizeof(float2);
     kp.NCB = kNCB448;   // K_B stats partials per stream
@@ -526,6 +526,33 @@ int fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes, const i
     return FC_EINVAL;
   return splice_impl(batch, n_tokens, row_bytes, src_map, cache, cache_ages, fresh, 1, 0, fresh_offsets, out,
                      out_ages, as_stream(stream));
+}
+
+int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, void* cache0,
+                      void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in, uint8_t* slot_out,
+                      const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* stream) {
+  if (batch < 1 || n_tokens < 1 || row_bytes < 16 || row_bytes % 16 || !src_map || !cache0 || !cache1 || !ages0 ||
+      !ages1 || !slot_in || !slot_out || !fresh)
+    return FC_EINVAL;
+  if (((reinterpret_cast<uintptr_t>(cache0) | reinterpret_cast<uintptr_t>(cache1) |
+        reinterpret_cast<uintptr_t>(fresh)) & 15) != 0)
+    return FC_EINVAL;
+  if (fresh_layout != FC_FRESH_DENSE && fresh_layout != FC_FRESH_COMPACT) return FC_EINVAL;
+  if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
+  const cudaStream_t st = as_stream(stream);
+  k_splice_plan<<<batch, 256, 0, st>>>(n_tokens, src_map, slot_in, slot_out);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int total = batch * n_tokens;
+  constexpr int UNR = 2;
+  int blocks = ((total + UNR - 1) / UNR + (FC_THREADS / 32) - 1) / (FC_THREADS / 32);
+  if (blocks > sms * 8) blocks = sms * 8;
+  k_splice_ip<UNR><<<blocks, FC_THREADS, 0, st>>>(
+      total, n_tokens, row_bytes / 16, src_map, reinterpret_cast<int4*>(cache0), reinterpret_cast<int4*>(cache1),
+      ages0, ages1, slot_in, slot_out, reinterpret_cast<const int4*>(fresh), fresh_layout == FC_FRESH_COMPACT,
+      fresh_rows, nullptr);
+  return launch_check();
 }
 
 int fc_splice_map(int32_t rows, int32_t cols, const int32_t* reuse_idx, int32_t k, int32_t dip, int32_t djp,

@@ -35,16 +35,27 @@ __device__ __forceinline__ float2 twid(const float2* __restrict__ t, int i) {
 // Per-role twiddles, loaded once per thread (ahead of the data they scale):
 // w1[k1-1] = w448^{r k1}, w3[m2-1] = w64^{m2 (r & 7)}.
 struct Tw {
-  float2 w1[6];
-  float2 w3[7];
+  float2 w1_[6];
+  float2 w3_[7];
+  __device__ __forceinline__ float2 w1(int k1) const { return w1_[k1 - 1]; }
+  __device__ __forceinline__ float2 w3(int m2) const { return w3_[m2 - 1]; }
+};
+
+// Twiddles read at their point of use (fewer live registers).
+struct TwLazy {
+  const float2* __restrict__ t448;
+  const float2* __restrict__ t64;
+  int r;
+  __device__ __forceinline__ float2 w1(int k1) const { return __ldg(t448 + (k1 - 1) * 64 + r); }
+  __device__ __forceinline__ float2 w3(int m2) const { return __ldg(t64 + (m2 - 1) * 8 + (r & 7)); }
 };
 
 __device__ __forceinline__ void load_tw(Tw& tw, int r, const float2* __restrict__ tw448,
                                         const float2* __restrict__ tw64) {
 #pragma unroll
-  for (int k1 = 1; k1 < 7; ++k1) tw.w1[k1 - 1] = __ldg(tw448 + (k1 - 1) * 64 + r);
+  for (int k1 = 1; k1 < 7; ++k1) tw.w1_[k1 - 1] = __ldg(tw448 + (k1 - 1) * 64 + r);
 #pragma unroll
-  for (int m2 = 1; m2 < 8; ++m2) tw.w3[m2 - 1] = __ldg(tw64 + (m2 - 1) * 8 + (r & 7));
+  for (int m2 = 1; m2 < 8; ++m2) tw.w3_[m2 - 1] = __ldg(tw64 + (m2 - 1) * 8 + (r & 7));
 }
 
 template <bool INV>
@@ -55,11 +66,11 @@ __device__ __forceinline__ float2 tw_apply(float2 v, float2 w) {
 // Forward-ordered FFT.  a[n1] = x[64 n1 + r] on entry (all 64 roles).  On
 // exit roles r < 56 hold X[k1 + 7 j1 + 56 j2] in b[j2].  S: this transform's
 // scratch.  Contains three __syncthreads (every thread must call).
-template <bool INV>
-__device__ __forceinline__ void fwd(float2 (&a)[7], float2 (&b)[8], float2* S, int r, const Tw& tw) {
+template <bool INV, class TW>
+__device__ __forceinline__ void fwd(float2 (&a)[7], float2 (&b)[8], float2* S, int r, const TW& tw) {
   DftOdd<7, INV>::run(a);
 #pragma unroll
-  for (int k1 = 1; k1 < 7; ++k1) a[k1] = tw_apply<INV>(a[k1], tw.w1[k1 - 1]);
+  for (int k1 = 1; k1 < 7; ++k1) a[k1] = tw_apply<INV>(a[k1], tw.w1(k1));
 #pragma unroll
   for (int k1 = 0; k1 < 7; ++k1) S[k1 * 72 + r] = a[k1];
   __syncthreads();
@@ -80,21 +91,21 @@ __device__ __forceinline__ void fwd(float2 (&a)[7], float2 (&b)[8], float2* S, i
 #pragma unroll
     for (int m2 = 0; m2 < 8; ++m2) b[m2] = S[k1 * 72 + 9 * lo + m2];
 #pragma unroll
-    for (int m2 = 1; m2 < 8; ++m2) b[m2] = tw_apply<INV>(b[m2], tw.w3[m2 - 1]);
+    for (int m2 = 1; m2 < 8; ++m2) b[m2] = tw_apply<INV>(b[m2], tw.w3(m2));
     Dft<8, INV>::run(b);
   }
 }
 
 // Transposed FFT: roles r < 56 hold X[k1 + 7 j1 + 56 j2] in b[j2] on entry;
 // on exit a[n1] = x[64 n1 + r] for all 64 roles.  Three __syncthreads.
-template <bool INV>
-__device__ __forceinline__ void inv(float2 (&b)[8], float2 (&a)[7], float2* S, int r, const Tw& tw) {
+template <bool INV, class TW>
+__device__ __forceinline__ void inv(float2 (&b)[8], float2 (&a)[7], float2* S, int r, const TW& tw) {
   const bool act = r < 56;
   const int k1 = r >> 3, lo = r & 7;
   if (act) {
     Dft<8, INV>::run(b);  // over j2 -> m2
 #pragma unroll
-    for (int m2 = 1; m2 < 8; ++m2) b[m2] = tw_apply<INV>(b[m2], tw.w3[m2 - 1]);
+    for (int m2 = 1; m2 < 8; ++m2) b[m2] = tw_apply<INV>(b[m2], tw.w3(m2));
 #pragma unroll
     for (int m2 = 0; m2 < 8; ++m2) S[k1 * 72 + 9 * lo + m2] = b[m2];
   }
@@ -113,7 +124,7 @@ __device__ __forceinline__ void inv(float2 (&b)[8], float2 (&a)[7], float2* S, i
 #pragma unroll
   for (int q = 0; q < 7; ++q) a[q] = S[q * 72 + r];
 #pragma unroll
-  for (int q = 1; q < 7; ++q) a[q] = tw_apply<INV>(a[q], tw.w1[q - 1]);
+  for (int q = 1; q < 7; ++q) a[q] = tw_apply<INV>(a[q], tw.w1(q));
   DftOdd<7, INV>::run(a);  // over k1 -> n1
 }
 
@@ -162,18 +173,20 @@ __device__ __forceinline__ double smem_luma(const unsigned char* px, int i) {
 }
 
 template <int FMT>
-__global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, const void* __restrict__ frames,
+__global__ void __launch_bounds__(448, 3) k448_rows_fwd(KParams kp, Dct14 dc, const void* __restrict__ frames,
                                                        int b0, int do_fft) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[2];
   constexpr int bpp = FMT == FC_FMT_RGB_F32 ? 12 : (FMT == FC_FMT_GRAY_F32 ? 4 : 8);
   const int s = blockIdx.x, bl = blockIdx.y, b = b0 + bl;
   const int t = threadIdx.x;
-  unsigned char* px = smem;                                          // stripe pixels
-  float2* zin = reinterpret_cast<float2*>(smem + kPxBytes448);       // [7][448]
-  float2* S = reinterpret_cast<float2*>(smem);                       // [7][504] (after phase 1)
-  double* part = reinterpret_cast<double*>(smem + 7 * f448::XR * 8); // [4][32 x 15]
-  double* ysq = part + 4 * 480;                                      // [9][32]
+  // one 73.5 KB region: the staged stripe, then (after every pixel is read)
+  // [zin 7x448 complex | DCT partials + corner squares | FFT scratch 7x504]
+  unsigned char* px = smem;
+  float2* zin = reinterpret_cast<float2*>(smem);                      // [7][448]
+  double* part = reinterpret_cast<double*>(smem + 7 * 448 * 8);       // [4][32 x 15]
+  double* ysq = part + 4 * 480;                                       // [9][32]
+  float2* S = reinterpret_cast<float2*>(smem + 7 * 448 * 8 + (4 * 480 + 288) * 8);  // [7][504]
 
   // ---- phase 0: stage the stripe with the TMA engine
   const size_t row0 = ((size_t)b * 448 + (size_t)s * 14) * 448;
@@ -194,16 +207,16 @@ __global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, co
   unsigned emax = 0u;
   double ref = 0.0;
   double s2 = 0.0, tu0 = 0.0, tu1 = 0.0, tu2 = 0.0;
+  float g32[14];
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     tma::bar_wait(&bar[half], 0);
     if (half == 0) ref = smem_luma<FMT>(px, 0);
-    double xv[7];
 #pragma unroll
     for (int x = 0; x < 7; ++x) {
       const int xx = half * 7 + x;
       const double v = smem_luma<FMT>(px, xx * 448 + t);
-      xv[x] = v;
+      g32[xx] = (float)v;
       vary |= (v != ref);
       emax = max(emax, (unsigned)__double2hiint(v) & 0x7ff00000u);
       s2 = fma(v, v, s2);
@@ -211,16 +224,12 @@ __global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, co
       tu1 = fma(dc.c[1][xx], v, tu1);
       tu2 = fma(dc.c[2][xx], v, tu2);
     }
-    // fp32 gray as packed row pairs (2g, 2g+1); rows 6,7 straddle the halves
-#pragma unroll
-    for (int x = 0; x < 7; ++x) {
-      const int xx = half * 7 + x;
-      if (xx & 1) zin[(xx >> 1) * 448 + t].y = (float)xv[x];
-      else        zin[(xx >> 1) * 448 + t].x = (float)xv[x];
-    }
   }
-  const int anyvary = __syncthreads_or(vary);  // also: pixels consumed
+  const int anyvary = __syncthreads_or(vary);  // also: every pixel has been read
   const int anybad = __syncthreads_or(emax == 0x7ff00000u);
+  // fp32 gray as packed row pairs (2g, 2g+1), over the consumed stripe
+#pragma unroll
+  for (int g = 0; g < 7; ++g) zin[g * 448 + t] = make_float2(g32[2 * g], g32[2 * g + 1]);
   // per-patch stride 15 (one pad double): phase-2 reads of 32 patches hit
   // 16 distinct bank pairs per half-warp
   {
@@ -267,8 +276,7 @@ __global__ void __launch_bounds__(448, 2) k448_rows_fwd(KParams kp, Dct14 dc, co
   float2 a[7], bv[8];
 #pragma unroll
   for (int n1 = 0; n1 < 7; ++n1) a[n1] = zin[g * 448 + 64 * n1 + r];
-  f448::Tw tw;
-  f448::load_tw(tw, r, kp.tw448, kp.tw64);
+  const f448::TwLazy tw{kp.tw448, kp.tw64, r};
   f448::fwd<false>(a, bv, S + g * f448::XR, r, tw);
   float2* zout = zin;  // zin fully consumed before fwd's first barrier
   if (r < 56) {

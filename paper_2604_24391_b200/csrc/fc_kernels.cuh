@@ -944,3 +944,82 @@ __global__ void k_state_reset(StreamHdr* hdr, int first, int count) {
     hdr[first + i] = h;
   }
 }
+
+// ------------------------------------------------------ in-place splice ----
+// Per stream: when every reused token's source is its own slot (zero
+// displacement, or nothing reused) the cache is updated in place — reused
+// rows stay where they are (age + 1) and only recomputed rows are written.
+// Otherwise the stream's spliced rows go to its other buffer (ping-pong).
+// slot_in[b] names the buffer holding stream b's cache; slot_out[b] the one
+// holding the result.
+__global__ void __launch_bounds__(256) k_splice_plan(int n_tokens, const int32_t* __restrict__ src_map,
+                                                     const uint8_t* __restrict__ slot_in,
+                                                     uint8_t* __restrict__ slot_out) {
+  const int b = blockIdx.x;
+  const int32_t* sm = src_map + (size_t)b * n_tokens;
+  int move = 0;
+  for (int p = threadIdx.x; p < n_tokens; p += blockDim.x) {
+    const int s = sm[p];
+    move |= (s >= 0 && s != p);
+  }
+  move = __syncthreads_or(move);
+  if (threadIdx.x == 0) slot_out[b] = move ? (uint8_t)(1 - slot_in[b]) : slot_in[b];
+}
+
+template <int UNR>
+__global__ void __launch_bounds__(FC_THREADS) k_splice_ip(int total, int n_tokens, int64_t row16,
+                                                          const int32_t* __restrict__ src_map,
+                                                          int4* cache0, int4* cache1, int64_t* ages0,
+                                                          int64_t* ages1, const uint8_t* __restrict__ slot_in,
+                                                          const uint8_t* __restrict__ slot_out,
+                                                          const int4* __restrict__ fresh, int compact,
+                                                          int fresh_rows, const int64_t* __restrict__ fresh_off) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int r0 = gw * UNR; r0 < total; r0 += nwarps * UNR) {
+    const int4* src[UNR];
+    int4* dst[UNR];
+    bool on[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int row = r0 + u;
+      const int rr = row < total ? row : r0;
+      const int bs = rr / n_tokens, p = rr - bs * n_tokens;
+      const int s = src_map[rr];
+      const int cur = slot_in[bs], nxt = slot_out[bs];
+      int4* cbuf = cur ? cache1 : cache0;
+      int4* nbuf = nxt ? cache1 : cache0;
+      int64_t* cage = cur ? ages1 : ages0;
+      int64_t* nage = nxt ? ages1 : ages0;
+      const size_t base = (size_t)bs * n_tokens;
+      const bool inplace_reuse = (cur == nxt) && s >= 0;  // row already in place
+      on[u] = row < total && !inplace_reuse;
+      if (s >= 0) {
+        src[u] = cbuf + (base + s) * row16;
+      } else {
+        const size_t f0 = fresh_off ? (size_t)fresh_off[bs] : (size_t)bs * fresh_rows;
+        src[u] = fresh + (f0 + (compact ? (-s - 1) : p)) * row16;
+      }
+      dst[u] = nbuf + (base + p) * row16;
+      if (row < total && lane == 0) nage[base + p] = s >= 0 ? cage[base + s] + 1 : 0;
+    }
+    for (int64_t c = lane; c < row16; c += 32 * 4) {
+      int4 v[UNR][4];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int64_t cc = c + 32 * m;
+          if (on[u] && cc < row16) v[u][m] = __ldcs(src[u] + cc);
+        }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int64_t cc = c + 32 * m;
+          if (on[u] && cc < row16) __stcs(dst[u] + cc, v[u][m]);
+        }
+    }
+  }
+}

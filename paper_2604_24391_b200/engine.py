@@ -213,6 +213,48 @@ def splice_packed(src_map, cache, cache_ages, fresh_values, fresh_offsets, out, 
     return out, out_ages
 
 
+class SpliceState:
+    """Ping-pong token cache for in-place splicing (``fc_splice_inplace``).
+
+    ``cache`` [2, B, N, D] and ``ages`` [2, B, N]; ``slot[b]`` names the
+    buffer that holds stream b's current cache (``current()`` gathers views).
+    """
+
+    def __init__(self, cache, ages):
+        if cache.dim() != 4 or cache.shape[0] != 2 or ages.shape != cache.shape[:3]:
+            raise ValueError("cache must be [2, B, N, D] and ages [2, B, N]")
+        self.cache, self.ages = cache, ages
+        B = cache.shape[1]
+        self.slots = [torch.zeros(B, dtype=torch.uint8, device=cache.device) for _ in range(2)]
+        self.k = 0
+
+    @property
+    def slot(self):
+        return self.slots[self.k]
+
+    def step(self, src_map, fresh, compact=False):
+        lib = nat.lib()
+        B, N = src_map.shape
+        row_bytes = self.cache.shape[-1] * self.cache.element_size()
+        if fresh.dtype != self.cache.dtype or fresh.shape[-1] != self.cache.shape[-1] or fresh.shape[0] != B:
+            raise ValueError("fresh must be [B, *, D] with the cache dtype")
+        sin, sout = self.slots[self.k], self.slots[1 - self.k]
+        rc = lib.fc_splice_inplace(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(self.cache[0]),
+                                   _ptr(self.cache[1]), _ptr(self.ages[0]), _ptr(self.ages[1]), _ptr(sin),
+                                   _ptr(sout), _ptr(fresh),
+                                   nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE, int(fresh.shape[1]),
+                                   _stream(self.cache.device))
+        nat.check(rc, "fc_splice_inplace")
+        self.k = 1 - self.k
+        return self.slot
+
+    def current(self):
+        """[B, N, D] tokens and [B, N] ages of every stream's current cache."""
+        idx = self.slot.long()
+        b = torch.arange(idx.numel(), device=idx.device)
+        return self.cache[idx, b], self.ages[idx, b]
+
+
 def splice_map(rows, cols, reuse_idx, di_patches, dj_patches, src_map=None, flag=None):
     """Device src_map for one stream from an ordered reuse list."""
     lib = nat.lib()

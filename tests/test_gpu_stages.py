@@ -308,3 +308,48 @@ def test_vit_cached_encoder_small(cuda):
                     if s >= 0:
                         assert torch.equal(cache_now[b, p], prev_h[b, s])
             assert float(cosine(y1, model(frames[1])).min()) > 0.5
+
+
+def test_inplace_splice_matches_oracle(cuda):
+    """fc_splice_inplace: zero-displacement streams update in place (reused
+    rows untouched), shifted streams ping-pong; results equal the oracle
+    splice bit for bit (bf16)."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    B, rows, cols, D = 5, 8, 8, 96
+    N = rows * cols
+    g = torch.Generator(device="cuda").manual_seed(1)
+    cache = torch.empty((2, B, N, D), dtype=torch.bfloat16, device="cuda")
+    cache[0] = torch.randn((B, N, D), generator=g, device="cuda").to(torch.bfloat16)
+    ages = torch.zeros((2, B, N), dtype=torch.int64, device="cuda")
+    ages[0] = torch.randint(0, 4, (B, N), generator=g, device="cuda")
+    st = fc.SpliceState(cache, ages)
+    rng = np.random.default_rng(7)
+    ref_tok = [cache[0, b].view(torch.int16).cpu().numpy().copy() for b in range(B)]
+    ref_age = [ages[0, b].cpu().numpy().copy() for b in range(B)]
+    for stepi in range(4):
+        src = np.empty((B, N), dtype=np.int32)
+        decs = []
+        for b in range(B):
+            dip, djp = [(0, 0), (1, 0), (0, -1), (0, 0), (2, 1)][(b + stepi) % 5]
+            al = [q for q in range(N) if 0 <= q // cols - dip < rows and 0 <= q % cols - djp < cols]
+            reuse = tuple(int(v) for v in rng.permutation(al)[: len(al) // 2])
+            flushed = (b + stepi) % 7 == 6
+            d = O.OracleDecision(step=1, flushed=flushed, sim_freq=1.0, displacement=(0, 0, dip, djp),
+                                 entropy=(0, 0, 0), alpha_t=0.5, k_reuse=0, k_candidate=0,
+                                 k_final=0 if flushed else len(reuse), reuse_set=() if flushed else reuse,
+                                 recompute_set=(), rows=rows, cols=cols, refresh_set=())
+            decs.append(d)
+            m = fc.splice_map(rows, cols, torch.tensor(d.reuse_set, dtype=torch.int32, device="cuda")
+                              if d.reuse_set else None, dip, djp)
+            src[b] = m.cpu().numpy()
+        fresh = torch.randn((B, N, D), generator=g, device="cuda").to(torch.bfloat16)
+        st.step(torch.from_numpy(src).cuda(), fresh, compact=False)
+        tok, age = st.current()
+        fr = fresh.view(torch.int16).cpu().numpy()
+        for b in range(B):
+            rec = [q for q in range(N) if q not in set(decs[b].reuse_set)]
+            exp, exp_age = O.splice(ref_tok[b], ref_age[b], decs[b], fr[b][rec])
+            assert np.array_equal(tok[b].view(torch.int16).cpu().numpy(), exp), (stepi, b)
+            assert np.array_equal(age[b].cpu().numpy(), exp_age), (stepi, b)
+            ref_tok[b], ref_age[b] = exp, exp_age
