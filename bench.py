@@ -394,18 +394,40 @@ def run_ours(a):
     torch.cuda.synchronize()
     ke = max(1, a.e2e_steps)
 
+    # copies on their own stream into double-buffered staging, so the H2D of
+    # step i+1 overlaps select + splice of step i; results come back per step
+    copy_s = torch.cuda.Stream(dev)
+    stages = [stage, torch.empty_like(stage)]
+    h2d_ev = [torch.cuda.Event(), torch.cuda.Event()]
+    use_ev = [torch.cuda.Event(), torch.cuda.Event()]
+    for e in use_ev:
+        e.record(stream)
+
+    def e2e_issue_copy(i):
+        k = i & 1
+        with torch.cuda.stream(copy_s):
+            copy_s.wait_event(use_ev[k])
+            stages[k].copy_(host[i % HR], non_blocking=True)
+            h2d_ev[k].record(copy_s)
+
     def e2e_step(i):
-        stage.copy_(host[i % HR], non_blocking=True)
-        out = eng.select(stage, cfg, refresh_shift=a.refresh_shift)
+        k = i & 1
+        stream.wait_event(h2d_ev[k])
+        out = eng.select(stages[k], cfg, refresh_shift=a.refresh_shift)
+        use_ev[k].record(stream)
         spl.step(out.src_map, fresh)
         res_host.copy_(out.results, non_blocking=True)
         map_host.copy_(out.src_map, non_blocking=True)
 
+    e2e_issue_copy(0)
     e2e_step(0)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    e2e_issue_copy(1)
     for i in range(1, ke + 1):
+        if i + 1 <= ke:
+            e2e_issue_copy(i + 1)
         e2e_step(i)
     e1.record(stream)
     barrier()
@@ -415,6 +437,49 @@ def run_ours(a):
     e2e_val = S * ke * world / (float(ems.item()) / 1e3)
     h2d = S * H * H * 3 * 4
     d2h = S * 136 + S * N * 4
+
+    # ---- single-stream step latency (select + splice), CUDA-graph replay:
+    # config 1 (224x224, fixed 50 % budget) and one config-2 stream (448x448)
+    latency = {}
+    if rank == 0:
+        for name, size, budget in (("config1_224", 224, (0.5, 0.5)), ("config2_448", 448, None)):
+            from paper_2604_24391_b200 import BudgetConfig
+            c1 = CacheConfig(patch_size=P) if budget is None else CacheConfig(patch_size=P, budget=BudgetConfig(*budget))
+            e1 = FreqCacheEngine(1, size, size, P, fmt="rgb", device=dev)
+            n1 = e1.n_tokens
+            fr1 = frames[:2, :1, :size, :size].contiguous() if size <= H else None
+            c1c = torch.randn((2, 1, n1, D), device=dev).to(torch.bfloat16)
+            a1 = torch.zeros((2, 1, n1), dtype=torch.int64, device=dev)
+            sp1 = SpliceState(c1c, a1)
+            fz = torch.randn((1, n1, D), device=dev).to(torch.bfloat16)
+            src_frame = torch.empty((1, size, size, 3), dtype=torch.float32, device=dev)
+            src_frame.copy_(fr1[0])
+            e1.select(src_frame, c1)
+            src_frame.copy_(fr1[1])
+            gs = torch.cuda.Stream(dev)
+            gs.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(gs):
+                for _ in range(3):
+                    o1 = e1.select(src_frame, c1)
+                    sp1.step(o1.src_map, fz)
+            torch.cuda.current_stream(dev).wait_stream(gs)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                o1 = e1.select(src_frame, c1)
+                sp1.step(o1.src_map, fz)
+            sp1.k = 0  # the captured step always reads slot buffer 0 -> 1
+            graph.replay()
+            torch.cuda.synchronize()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 200
+            q0.record()
+            for _ in range(reps):
+                graph.replay()
+            q1.record()
+            torch.cuda.synchronize()
+            latency[name] = {"ms_per_step": q0.elapsed_time(q1) / reps, "streams": 1, "size": size,
+                             "tokens": n1, "path": "CUDA graph: fc_select + fc_splice_inplace"}
+        latency["reference_paper_a100_ms"] = 2.54
 
     # ---- CPU baseline (rank 0, N == 1 only)
     cpu = None
@@ -439,8 +504,10 @@ def run_ours(a):
             "roofline": roofline, "roofline_step": roofline_step, "kernels": kernels,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": ke, "path": "pinned host frames -> fc_select -> fc_splice -> results to host"},
+                    "steps": ke, "path": "pinned host frames -> (copy stream, double-buffered) fc_select -> "
+                                         "fc_splice_inplace -> results + splice map to pinned host"},
             "gpu_launches": gpu_launches,
+            "latency": latency,
             "clocks": clocks.summary(),
             "decisions": {"reuse_ratio_last_step": reuse_ratio, "flush_rate_last_step": flush_rate},
         }
