@@ -203,11 +203,12 @@ int  fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes,
  * reused rows are not touched (age + 1) and only recomputed rows are written.
  * Any other stream is spliced into its other buffer.  slot_out[b] receives the
  * buffer now holding the result.  Rows must be 16-byte multiples/aligned.   */
+int64_t fc_splice_inplace_scratch_bytes(int32_t batch, int32_t n_tokens);
 int  fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                        const int32_t* src_map, void* cache0, void* cache1,
                        int64_t* ages0, int64_t* ages1, const uint8_t* slot_in,
                        uint8_t* slot_out, const void* fresh, int32_t fresh_layout,
-                       int32_t fresh_rows, void* cuda_stream);
+                       int32_t fresh_rows, void* scratch, void* cuda_stream);
 
 /* Build src_map for one stream from an ordered reuse list (fusion.py:481-504).
  * flag (device int32, may be NULL) receives FC_EBOUNDS on an out-of-bounds

@@ -43,7 +43,7 @@ EXPORTS = (
     "fc_state_reset", "fc_select", "fc_select_profile", "fc_patch_energy", "fc_splice",
     "fc_splice_map", "fc_stage_workspace_bytes", "fc_amp_cosine", "fc_spectral_sums",
     "fc_refresh_mask", "fc_topk_ascending", "fc_render_masks", "fc_splice_packed",
-    "fc_splice_inplace",
+    "fc_splice_inplace", "fc_splice_inplace_scratch_bytes",
 )
 
 
@@ -115,7 +115,8 @@ def load(path=None):
         "fc_stage_workspace_bytes": (i64, []),
         "fc_render_masks": (C.c_int, [i32, i32, vp, vp, vp, vp, vp]),
         "fc_splice_packed": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
-        "fc_splice_inplace": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp]),
+        "fc_splice_inplace": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]),
+        "fc_splice_inplace_scratch_bytes": (i64, [i32, i32]),
         "fc_amp_cosine": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
         "fc_spectral_sums": (C.c_int, [vp, i64, i32, vp, vp, vp, vp]),
         "fc_refresh_mask": (C.c_int, [vp, i64, C.c_double, vp, vp, vp, vp]),

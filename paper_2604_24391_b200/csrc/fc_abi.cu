@@ -528,11 +528,15 @@ int fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes, const i
                      out_ages, as_stream(stream));
 }
 
+int64_t fc_splice_inplace_scratch_bytes(int32_t batch, int32_t n_tokens) {
+  return (int64_t)batch * n_tokens * 4 + (int64_t)batch * 4 + 256;
+}
+
 int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, void* cache0,
                       void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in, uint8_t* slot_out,
-                      const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* stream) {
+                      const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* scratch, void* stream) {
   if (batch < 1 || n_tokens < 1 || row_bytes < 16 || row_bytes % 16 || !src_map || !cache0 || !cache1 || !ages0 ||
-      !ages1 || !slot_in || !slot_out || !fresh)
+      !ages1 || !slot_in || !slot_out || !fresh || !scratch)
     return FC_EINVAL;
   if (((reinterpret_cast<uintptr_t>(cache0) | reinterpret_cast<uintptr_t>(cache1) |
         reinterpret_cast<uintptr_t>(fresh)) & 15) != 0)
@@ -540,7 +544,9 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
   if (fresh_layout != FC_FRESH_DENSE && fresh_layout != FC_FRESH_COMPACT) return FC_EINVAL;
   if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
   const cudaStream_t st = as_stream(stream);
-  k_splice_plan<<<batch, 256, 0, st>>>(n_tokens, src_map, slot_in, slot_out);
+  int32_t* rows = reinterpret_cast<int32_t*>(scratch);
+  int32_t* counts = rows + (size_t)batch * n_tokens;
+  k_splice_plan<<<batch, 256, 0, st>>>(n_tokens, src_map, slot_in, slot_out, ages0, ages1, rows, counts);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -550,8 +556,8 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
   if (blocks > sms * 8) blocks = sms * 8;
   k_splice_ip<UNR><<<blocks, FC_THREADS, 0, st>>>(
       total, n_tokens, row_bytes / 16, src_map, reinterpret_cast<int4*>(cache0), reinterpret_cast<int4*>(cache1),
-      ages0, ages1, slot_in, slot_out, reinterpret_cast<const int4*>(fresh), fresh_layout == FC_FRESH_COMPACT,
-      fresh_rows, nullptr);
+      ages0, ages1, slot_in, slot_out, rows, counts, reinterpret_cast<const int4*>(fresh),
+      fresh_layout == FC_FRESH_COMPACT, fresh_rows);
   return launch_check();
 }
 

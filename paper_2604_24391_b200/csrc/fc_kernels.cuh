@@ -948,22 +948,61 @@ __global__ void k_state_reset(StreamHdr* hdr, int first, int count) {
 // ------------------------------------------------------ in-place splice ----
 // Per stream: when every reused token's source is its own slot (zero
 // displacement, or nothing reused) the cache is updated in place — reused
-// rows stay where they are (age + 1) and only recomputed rows are written.
-// Otherwise the stream's spliced rows go to its other buffer (ping-pong).
-// slot_in[b] names the buffer holding stream b's cache; slot_out[b] the one
-// holding the result.
+// rows stay where they are (age + 1, done here) and only recomputed rows are
+// copied.  Otherwise every row of the stream goes to its other buffer
+// (ping-pong).  slot_in[b] names the buffer holding stream b's cache,
+// slot_out[b] the one holding the result.  The plan kernel also compacts the
+// rows to copy (ascending) so the copy kernel's warps only see real work.
 __global__ void __launch_bounds__(256) k_splice_plan(int n_tokens, const int32_t* __restrict__ src_map,
                                                      const uint8_t* __restrict__ slot_in,
-                                                     uint8_t* __restrict__ slot_out) {
+                                                     uint8_t* __restrict__ slot_out, int64_t* ages0,
+                                                     int64_t* ages1, int32_t* __restrict__ rows,
+                                                     int32_t* __restrict__ counts) {
+  __shared__ int redi[8];
   const int b = blockIdx.x;
-  const int32_t* sm = src_map + (size_t)b * n_tokens;
+  const size_t base = (size_t)b * n_tokens;
+  const int32_t* sm = src_map + base;
   int move = 0;
   for (int p = threadIdx.x; p < n_tokens; p += blockDim.x) {
     const int s = sm[p];
     move |= (s >= 0 && s != p);
   }
   move = __syncthreads_or(move);
-  if (threadIdx.x == 0) slot_out[b] = move ? (uint8_t)(1 - slot_in[b]) : slot_in[b];
+  const int cur = slot_in[b];
+  if (threadIdx.x == 0) slot_out[b] = move ? (uint8_t)(1 - cur) : (uint8_t)cur;
+  int32_t* rl = rows + base;
+  if (move) {
+    for (int p = threadIdx.x; p < n_tokens; p += blockDim.x) rl[p] = p;
+    if (threadIdx.x == 0) counts[b] = n_tokens;
+    return;
+  }
+  int64_t* ag = (cur ? ages1 : ages0) + base;
+  // ascending compaction of recomputed rows; reused rows age in place
+  const int per = (n_tokens + blockDim.x - 1) / blockDim.x;
+  const int p0 = threadIdx.x * per, p1 = min(n_tokens, p0 + per);
+  int cnt = 0;
+  for (int p = p0; p < p1; ++p) {
+    if (sm[p] < 0) ++cnt;
+    else ag[p] += 1;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) redi[wid] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int w = 0; w < nw; ++w) { const int t = redi[w]; redi[w] = acc; acc += t; }
+    counts[b] = acc;
+  }
+  __syncthreads();
+  int run = redi[wid] + incl - cnt;
+  for (int p = p0; p < p1; ++p)
+    if (sm[p] < 0) rl[run++] = p;
 }
 
 template <int UNR>
@@ -972,8 +1011,10 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice_ip(int total, int n_token
                                                           int4* cache0, int4* cache1, int64_t* ages0,
                                                           int64_t* ages1, const uint8_t* __restrict__ slot_in,
                                                           const uint8_t* __restrict__ slot_out,
+                                                          const int32_t* __restrict__ rows,
+                                                          const int32_t* __restrict__ counts,
                                                           const int4* __restrict__ fresh, int compact,
-                                                          int fresh_rows, const int64_t* __restrict__ fresh_off) {
+                                                          int fresh_rows) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -983,26 +1024,30 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice_ip(int total, int n_token
     bool on[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int row = r0 + u;
-      const int rr = row < total ? row : r0;
-      const int bs = rr / n_tokens, p = rr - bs * n_tokens;
-      const int s = src_map[rr];
+      const int task = r0 + u;
+      const int tt = task < total ? task : r0;
+      const int bs = tt / n_tokens, k = tt - bs * n_tokens;
+      on[u] = task < total && k < counts[bs];
+      src[u] = fresh;
+      dst[u] = cache0;
+      if (!on[u]) continue;
+      const size_t base = (size_t)bs * n_tokens;
+      const int p = rows[base + k];
+      const int s = src_map[base + p];
       const int cur = slot_in[bs], nxt = slot_out[bs];
       int4* cbuf = cur ? cache1 : cache0;
       int4* nbuf = nxt ? cache1 : cache0;
-      int64_t* cage = cur ? ages1 : ages0;
-      int64_t* nage = nxt ? ages1 : ages0;
-      const size_t base = (size_t)bs * n_tokens;
-      const bool inplace_reuse = (cur == nxt) && s >= 0;  // row already in place
-      on[u] = row < total && !inplace_reuse;
       if (s >= 0) {
         src[u] = cbuf + (base + s) * row16;
       } else {
-        const size_t f0 = fresh_off ? (size_t)fresh_off[bs] : (size_t)bs * fresh_rows;
-        src[u] = fresh + (f0 + (compact ? (-s - 1) : p)) * row16;
+        src[u] = fresh + ((size_t)bs * fresh_rows + (compact ? (-s - 1) : p)) * row16;
       }
       dst[u] = nbuf + (base + p) * row16;
-      if (row < total && lane == 0) nage[base + p] = s >= 0 ? cage[base + s] + 1 : 0;
+      if (lane == 0) {
+        int64_t* cage = cur ? ages1 : ages0;
+        int64_t* nage = nxt ? ages1 : ages0;
+        nage[base + p] = s >= 0 ? cage[base + s] + 1 : 0;
+      }
     }
     for (int64_t c = lane; c < row16; c += 32 * 4) {
       int4 v[UNR][4];

@@ -227,6 +227,8 @@ class SpliceState:
         B = cache.shape[1]
         self.slots = [torch.zeros(B, dtype=torch.uint8, device=cache.device) for _ in range(2)]
         self.k = 0
+        nb = nat.lib().fc_splice_inplace_scratch_bytes(int(B), int(cache.shape[2]))
+        self.scratch = torch.empty(nb, dtype=torch.uint8, device=cache.device)
 
     @property
     def slot(self):
@@ -243,7 +245,7 @@ class SpliceState:
                                    _ptr(self.cache[1]), _ptr(self.ages[0]), _ptr(self.ages[1]), _ptr(sin),
                                    _ptr(sout), _ptr(fresh),
                                    nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE, int(fresh.shape[1]),
-                                   _stream(self.cache.device))
+                                   _ptr(self.scratch), _stream(self.cache.device))
         nat.check(rc, "fc_splice_inplace")
         self.k = 1 - self.k
         return self.slot

@@ -289,3 +289,33 @@ def test_phase_correlation_and_energy(cuda):
     frame = rng.random((64, 64))
     e = fc.patch_energy(fc.PatchGrid(frame, 8)).energies
     np.testing.assert_allclose(e, O.block_energy(frame, 8), rtol=1e-10, atol=1e-14)
+
+
+def test_config2_sweep_16_streams(cuda):
+    """Wider parity sweep on the fast path: 16 config-2 streams x 13 steps
+    (one scene cut), batched, refresh rule on; every decision checked."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.api import decision_from_device
+    from paper_2604_24391_b200.synth import stream_frames
+    S, T = 16, 14
+    frames = np.stack([stream_frames(2500, s, T, 448, 448) for s in range(S)], axis=1)
+    c, oc = _cfg(patch_size=14)
+    oc.refresh_shift = 1
+    eng = fc.FreqCacheEngine(S, 448, 448, 14, fmt="rgb")
+    rep = ParityReport()
+    n_exact = 0
+    for t in range(T):
+        out = eng.select(torch.from_numpy(np.ascontiguousarray(frames[t])).cuda(), c, refresh_shift=1)
+        if t == 0:
+            continue
+        res = out.host_results()
+        en = out.energy.cpu().numpy()
+        ri, rc, rm = out.reuse_idx.cpu().numpy(), out.recompute_idx.cpu().numpy(), out.refresh_mask.cpu().numpy()
+        for s in range(S):
+            d = decision_from_device(res[s], ri[s], rc[s], rm[s], step=t)
+            o = O.decide(frames[t - 1, s], frames[t, s], oc, step=t)
+            compare(d, o, oc, energies=en[s], rep=rep)
+            n_exact += tuple(d.reuse_set) == o.reuse_set and tuple(d.refresh_set) == o.refresh_set
+    assert rep.ok, rep.errors
+    print(f"config-2 sweep: {n_exact}/{S * (T - 1)} decisions identical to the oracle; exemptions {rep.exemptions}")
