@@ -546,6 +546,98 @@ __device__ __forceinline__ bool key_less(double ea, int ia, double eb, int ib) {
   return ea < eb || (ea == eb && ia < ib);
 }
 
+// Bitonic sort of (E, index) keys in shared memory, one CTA.
+__device__ void bitonic_smem(double* ke, int* ki, int NP2) {
+  for (int k = 2; k <= NP2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < NP2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double ea = ke[i], eb = ke[ixj];
+          const int ia = ki[i], ib = ki[ixj];
+          const bool up = (i & k) == 0;
+          const bool swap = up ? key_less(eb, ib, ea, ia) : key_less(ea, ia, eb, ib);
+          if (swap) { ke[i] = eb; ke[ixj] = ea; ki[i] = ib; ki[ixj] = ia; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Bitonic steps j = jmax..1 (jmax <= 32) on the 64 keys a warp holds in
+// registers: lane L has elements base+L (slot 0) and base+L+32 (slot 1).
+// Distance 32 pairs the two slots of a lane; smaller distances pair lanes
+// (xor shuffles).  No barriers.
+__device__ __forceinline__ void warp_bitonic(double (&e)[2], int (&x)[2], int base, int k, int jmax) {
+  const int lane = threadIdx.x & 31;
+  for (int j = jmax; j > 0; j >>= 1) {
+    if (j == 32) {
+      const bool up = ((base + lane) & k) == 0;
+      const bool gt = key_less(e[1], x[1], e[0], x[0]);  // slot0 > slot1
+      if (up == gt) {
+        const double te = e[0]; e[0] = e[1]; e[1] = te;
+        const int tx = x[0]; x[0] = x[1]; x[1] = tx;
+      }
+    } else {
+#pragma unroll
+      for (int sl = 0; sl < 2; ++sl) {
+        const double oe = __shfl_xor_sync(0xffffffffu, e[sl], j);
+        const int ox = __shfl_xor_sync(0xffffffffu, x[sl], j);
+        const int i = base + lane + 32 * sl;
+        const bool up = (i & k) == 0;
+        const bool low = (lane & j) == 0;             // this element has the smaller index
+        const bool other_less = key_less(oe, ox, e[sl], x[sl]);
+        // ascending pair: low keeps the min, high keeps the max
+        const bool take = (up == low) ? other_less : !other_less;
+        if (take) { e[sl] = oe; x[sl] = ox; }
+      }
+    }
+  }
+}
+
+// Same sort with register/shuffle stages for distances < 64 and shared
+// memory only for the cross-warp distances: 10 barrier phases at N = 1024
+// instead of 55.  NP2 >= 64, power of two.
+__device__ void bitonic_hybrid(double* ke, int* ki, int NP2) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nseg = NP2 / 64;
+  // phase A: every 64-key segment sorted by its warp (k = 2 .. 64)
+  for (int sg = wid; sg < nseg; sg += nw) {
+    const int base = sg * 64;
+    double e[2] = {ke[base + lane], ke[base + lane + 32]};
+    int x[2] = {ki[base + lane], ki[base + lane + 32]};
+    for (int k = 2; k <= 64; k <<= 1) warp_bitonic(e, x, base, k, k >> 1);
+    ke[base + lane] = e[0]; ke[base + lane + 32] = e[1];
+    ki[base + lane] = x[0]; ki[base + lane + 32] = x[1];
+  }
+  __syncthreads();
+  for (int k = 128; k <= NP2; k <<= 1) {
+    for (int j = k >> 1; j >= 64; j >>= 1) {
+      for (int i = threadIdx.x; i < NP2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double ea = ke[i], eb = ke[ixj];
+          const int ia = ki[i], ib = ki[ixj];
+          const bool up = (i & k) == 0;
+          const bool swap = up ? key_less(eb, ib, ea, ia) : key_less(ea, ia, eb, ib);
+          if (swap) { ke[i] = eb; ke[ixj] = ea; ki[i] = ib; ki[ixj] = ia; }
+        }
+      }
+      __syncthreads();
+    }
+    for (int sg = wid; sg < nseg; sg += nw) {
+      const int base = sg * 64;
+      double e[2] = {ke[base + lane], ke[base + lane + 32]};
+      int x[2] = {ki[base + lane], ki[base + lane + 32]};
+      warp_bitonic(e, x, base, k, 32);
+      ke[base + lane] = e[0]; ke[base + lane + 32] = e[1];
+      ki[base + lane] = x[0]; ki[base + lane + 32] = x[1];
+    }
+    __syncthreads();
+  }
+}
+
 // Decision for one stream (fusion.py:121-242 selection; 245-262 invariants
 // hold by construction).  Scalars in thread 0, per-token work spread.
 __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config cfg,
@@ -755,21 +847,8 @@ __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config
   const int kfinal = sh_kfinal;
   if (kfinal > 0) {
     // ascending (E, index) bitonic sort (fusion.py:104-115)
-    for (int k = 2; k <= NP2; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < NP2; i += blockDim.x) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const double ea = ke[i], eb = ke[ixj];
-            const int ia = ki[i], ib = ki[ixj];
-            const bool up = (i & k) == 0;
-            const bool swap = up ? key_less(eb, ib, ea, ia) : key_less(ea, ia, eb, ib);
-            if (swap) { ke[i] = eb; ke[ixj] = ea; ki[i] = ib; ki[ixj] = ia; }
-          }
-        }
-        __syncthreads();
-      }
-    }
+    if (NP2 >= 64) bitonic_hybrid(ke, ki, NP2);
+    else bitonic_smem(ke, ki, NP2);
     for (int r = threadIdx.x; r < kfinal; r += blockDim.x) reuse[ki[r]] = 1;
   }
   __syncthreads();
