@@ -47,6 +47,8 @@ struct fc_plan {
   size_t lane_stride = 0;              // workspace bytes per lane (T1 + T2)
   bool persistent = false;             // fast path: persistent K_B / K_C (FC_PERSISTENT=1)
   int gridB = 0, gridC = 0;            // persistent grid sizes (SMs x occupancy)
+  void* fnB = nullptr;                 // K_B / K_C variants (occupancy x twiddle mode)
+  void* fnC = nullptr;
   float2* d_twW = nullptr;
   float2* d_twH = nullptr;
   double* d_dct = nullptr;
@@ -196,14 +198,16 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
         const int gb = nb * kNCB448 < pl->gridB ? nb * kNCB448 : pl->gridB;
         k448_cols_p<<<gb, 64 * kBC, kSmemBP, ls>>>(kl, b0, nb);
       } else {
-        k448_cols<<<dim3(kNCB448, nb), 64 * kBC, pl->smemB, ls>>>(kl, b0);
+        auto fb = (void (*)(KParams, int))pl->fnB;
+        fb<<<dim3(kNCB448, nb), 64 * kBC, pl->smemB, ls>>>(kl, b0);
       }
       if (rec) rec->mark(st, 1);
       if (pl->persistent) {
         const int gc = nb * kNRG448 < pl->gridC ? nb * kNRG448 : pl->gridC;
         k448_rows_inv_p<<<gc, 64 * kBP, kSmemCP, ls>>>(kl, b0, nb);
       } else {
-        k448_rows_inv<<<dim3(kNRG448, nb), 64 * kBP, pl->smemC, ls>>>(kl, b0);
+        auto fc = (void (*)(KParams, int))pl->fnC;
+        fc<<<dim3(kNRG448, nb), 64 * kBP, pl->smemC, ls>>>(kl, b0);
       }
       if (rec) rec->mark(st, 2);
     }
@@ -364,8 +368,15 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
   if (rc == FC_OK) {
     if (pl->fast) {
       rc = set_smem(sel_fast_rows_fwd(g.format), pl->smemA);
-      if (rc == FC_OK) rc = set_smem((void*)k448_cols, pl->smemB);
-      if (rc == FC_OK) rc = set_smem((void*)k448_rows_inv, pl->smemC);
+      // occupancy variants: FC_OCC_B / FC_OCC_C = target CTAs per SM (register
+      // cap), twiddles read at use when the cap is tight
+      const int ob = env_int("FC_OCC_B", 3, 3, 6), oc = env_int("FC_OCC_C", 6, 3, 6);
+      pl->fnB = ob == 6 ? (void*)k448_cols<6, true> : ob == 5 ? (void*)k448_cols<5, true>
+              : ob == 3 ? (void*)k448_cols<4, true> : (void*)k448_cols<4, false>;
+      pl->fnC = oc == 6 ? (void*)k448_rows_inv<6, true> : oc == 5 ? (void*)k448_rows_inv<5, true>
+              : oc == 3 ? (void*)k448_rows_inv<4, true> : (void*)k448_rows_inv<4, false>;
+      if (rc == FC_OK) rc = set_smem(pl->fnB, pl->smemB);
+      if (rc == FC_OK) rc = set_smem(pl->fnC, pl->smemC);
       if (rc == FC_OK) rc = set_smem((void*)k448_cols_p, kSmemBP);
       if (rc == FC_OK) rc = set_smem((void*)k448_rows_inv_p, kSmemCP);
       if (rc == FC_OK) {

@@ -141,6 +141,18 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
+template <bool LAZY> struct TwSel;
+template <> struct TwSel<true> {
+  __device__ __forceinline__ static f448::TwLazy make(const KParams& kp, int r) { return {kp.tw448, kp.tw64, r}; }
+};
+template <> struct TwSel<false> {
+  __device__ __forceinline__ static f448::Tw make(const KParams& kp, int r) {
+    f448::Tw t;
+    f448::load_tw(t, r, kp.tw448, kp.tw64);
+    return t;
+  }
+};
+
 struct Dct14 {
   double c[3][14];  // orthonormal DCT-II rows u < 3 for P = 14
 };
@@ -318,7 +330,8 @@ constexpr int kStBlock = 64 * kBC * 8 * 8;   // bytes
 constexpr int kXCB = 516;                    // scratch stride, 4 interleaved transforms
 constexpr int kScratchB = kBC * kXCB * 8;
 
-__global__ void __launch_bounds__(64 * kBC, 4) k448_cols(KParams kp, int b0) {
+template <int MINB, bool LAZY>
+__global__ void __launch_bounds__(64 * kBC, MINB) k448_cols(KParams kp, int b0) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ double red[16 * 4];
@@ -340,8 +353,7 @@ __global__ void __launch_bounds__(64 * kBC, 4) k448_cols(KParams kp, int b0) {
     tma::load_tile(t1, kp.T + ((size_t)bl * kNCB448 + cb) * 448 * kBC, kT1Block, &bar[0]);
     if (valid) tma::load_tile(prev, stg, kStBlock, &bar[1]);
   }
-  f448::Tw tw;
-  f448::load_tw(tw, r, kp.tw448, kp.tw64);
+  const auto tw = TwSel<LAZY>::make(kp, r);
   tma::bar_wait(&bar[0], 0);
   float2 a[7], v[8];
 #pragma unroll
@@ -431,7 +443,8 @@ __global__ void __launch_bounds__(64 * kBC, 4) k448_cols(KParams kp, int b0) {
 // The rows of T2 (contiguous) arrive by one TMA bulk copy.
 constexpr int kT2Rows = 2 * kBP * 224 * 8;  // bytes
 
-__global__ void __launch_bounds__(64 * kBP, 4) k448_rows_inv(KParams kp, int b0) {
+template <int MINB, bool LAZY>
+__global__ void __launch_bounds__(64 * kBP, MINB) k448_rows_inv(KParams kp, int b0) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ PeakKey redk[16];
@@ -445,8 +458,7 @@ __global__ void __launch_bounds__(64 * kBP, 4) k448_rows_inv(KParams kp, int b0)
     tma::load_tile(tin, kp.T2 + ((size_t)bl * 448 + y0) * 224, kT2Rows, &bar);  // same thread: ordered
   }
   const int g = t >> 6, r = t & 63;
-  f448::Tw tw;
-  f448::load_tw(tw, r, kp.tw448, kp.tw64);
+  const auto tw = TwSel<LAZY>::make(kp, r);
   const bool valid = kp.hdr[b].valid != 0;
   __syncthreads();  // barrier initialised
   tma::bar_wait(&bar, 0);  // also when cold: the CTA must not exit with a copy in flight
