@@ -251,7 +251,7 @@ def run_ours(a):
     # of step t+1.  Select outputs are double-buffered; splice(t-2) must have
     # consumed a buffer before select(t) rewrites it.
     main = torch.cuda.current_stream(dev)
-    side = torch.cuda.Stream(dev, priority=-1)  # splice CTAs jump the select queue
+    side = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_SIDE_PRIO", "-1")))  # splice CTAs jump the select queue
     outs = [eng.out, eng.new_output()]
     sel_ev = [torch.cuda.Event(), torch.cuda.Event()]
     spl_ev = [torch.cuda.Event(), torch.cuda.Event()]

@@ -23,6 +23,7 @@
 #include <stdint.h>
 
 #include "fc_fft.cuh"
+#include "fc_tma.cuh"
 #include "../../include/freqcache_b200.h"
 
 #define FC_CB 8
@@ -1053,8 +1054,10 @@ __global__ void __launch_bounds__(256) k_splice_plan(int n_tokens, const int32_t
   if (move) {
     for (int p = threadIdx.x; p < n_tokens; p += blockDim.x) rl[p] = p;
     if (threadIdx.x == 0) counts[b] = n_tokens;
+    if (b == 0 && threadIdx.x == 0) counts[gridDim.x] = 0;  // bulk copier's work counter
     return;
   }
+  if (b == 0 && threadIdx.x == 0) counts[gridDim.x] = 0;
   int64_t* ag = (cur ? ages1 : ages0) + base;
   // ascending compaction of recomputed rows; reused rows age in place
   const int per = (n_tokens + blockDim.x - 1) / blockDim.x;
@@ -1146,4 +1149,90 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice_ip(int total, int n_token
         }
     }
   }
+}
+
+// Bulk-copy variant of k_splice_ip for running beside the select kernels:
+// one warp per CTA, NL lanes each own two row slots in shared memory and
+// move rows with the TMA engine (global -> shared -> global), so a CTA keeps
+// 2 * NL rows in flight while issuing a handful of instructions per row.
+// Rows are claimed dynamically (one atomic per row) so CTAs that start late,
+// behind a resident select kernel, simply take less work.  Task t maps to
+// (stream, k) through an exclusive scan of counts[] built per CTA.
+template <int NL>
+__global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, int row_bytes,
+                                                       const int32_t* __restrict__ src_map, char* cache0,
+                                                       char* cache1, int64_t* ages0, int64_t* ages1,
+                                                       const uint8_t* __restrict__ slot_in,
+                                                       const uint8_t* __restrict__ slot_out,
+                                                       const int32_t* __restrict__ rows, int32_t* counts,
+                                                       const char* __restrict__ fresh, int compact, int fresh_rows) {
+  extern __shared__ __align__(128) unsigned char smem[];  // [NL][2][row_bytes] | offs[batch + 1]
+  __shared__ __align__(8) uint64_t bar[NL * 2];
+  const int lane = threadIdx.x;
+  int* offs = reinterpret_cast<int*>(smem + (size_t)NL * 2 * row_bytes);
+  if (lane < NL * 2) tma::bar_init(&bar[lane], 1);
+  // exclusive scan of counts (lane-contiguous segments)
+  const int per = (batch + 31) / 32, q0 = lane * per, q1 = min(batch, q0 + per);
+  int sum = 0;
+  for (int q = q0; q < q1; ++q) sum += counts[q];
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int run = incl - sum;
+  for (int q = q0; q < q1; ++q) { offs[q] = run; run += counts[q]; }
+  const int tot = __shfl_sync(0xffffffffu, incl, 31);
+  if (lane == 31) offs[batch] = tot;
+  __syncwarp();
+  if (lane >= NL) return;
+  int* work = counts + batch;
+  unsigned char* slot0 = smem + (size_t)lane * 2 * row_bytes;
+  bool pend = false;
+  char* pdst = nullptr;
+  int pslot = 0;
+  uint32_t pphase = 0;
+  for (int it = 0;; ++it) {
+    const int task = atomicAdd(work, 1);
+    const bool have = task < tot;
+    const int sl = it & 1;
+    unsigned char* buf = slot0 + sl * row_bytes;
+    char* dst = nullptr;
+    if (have) {
+      // stream of this task: last b with offs[b] <= task
+      int lo = 0, hi = batch - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (offs[mid] <= task) lo = mid; else hi = mid - 1;
+      }
+      const int bs = lo, k = task - offs[bs];
+      const size_t base = (size_t)bs * n_tokens;
+      const int p = rows[base + k];
+      const int s = src_map[base + p];
+      const int cur = slot_in[bs], nxt = slot_out[bs];
+      const char* cbuf = cur ? cache1 : cache0;
+      char* nbuf = nxt ? cache1 : cache0;
+      const char* src = s >= 0 ? cbuf + (base + s) * row_bytes
+                               : fresh + ((size_t)bs * fresh_rows + (compact ? (-s - 1) : p)) * row_bytes;
+      dst = nbuf + (base + p) * row_bytes;
+      const int64_t* cage = cur ? ages1 : ages0;
+      int64_t* nage = nxt ? ages1 : ages0;
+      nage[base + p] = s >= 0 ? cage[base + s] + 1 : 0;
+      // this slot's previous store (two rows back) must have left shared memory
+      tma::bulk_wait_read0();
+      tma::bar_expect(&bar[lane * 2 + sl], row_bytes);
+      tma::bulk_g2s(buf, src, row_bytes, &bar[lane * 2 + sl]);
+    }
+    if (pend) {
+      tma::bar_wait(&bar[lane * 2 + pslot], pphase);
+      tma::bulk_s2g(pdst, slot0 + pslot * row_bytes, row_bytes);
+    }
+    if (!have) break;
+    pend = true;
+    pdst = dst;
+    pslot = sl;
+    pphase = (it >> 1) & 1;
+  }
+  tma::bulk_wait0();
 }
