@@ -217,6 +217,20 @@ int  fc_splice_map(int32_t rows, int32_t cols, const int32_t* reuse_idx,
                    int32_t k, int32_t di_patches, int32_t dj_patches,
                    int32_t* src_map, int32_t* flag, void* cuda_stream);
 
+/* ---- comparison baselines (compare.py:23-52, the paper's two position-wise
+ * policies).  For B frame pairs (prev[b], curr[b]) in geom's format, per patch
+ * (row-major, [B][N] float64): visual_cos = cosine of the raw gray pixels,
+ * naive_cos = cosine of the |fft2| amplitude spectra of the P x P patches;
+ * a pair with a zero norm scores 0.  2 <= patch_size <= 32.  Replaces
+ * compare.py:41-52 + 90-95 (_token_stack with the raw-pixel token_fn,
+ * _patch_amplitudes, _position_cosines).                                    */
+int  fc_compare_cosines(const fc_geometry* geom, const void* prev, const void* curr,
+                        double* visual_cos, double* naive_cos, void* cuda_stream);
+/* Row-wise cosine of two [n][d] float64 stacks (compare.py:28-38), e.g. a
+ * custom token_fn's vectors.                                                */
+int  fc_row_cosines(int64_t n, int64_t d, const double* a, const double* b,
+                    double* out, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

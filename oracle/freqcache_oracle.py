@@ -409,3 +409,86 @@ def decision_margins(d: OracleDecision, cfg: OracleConfig):
         "energy_floor": floor,
         "psi_one": abs(d.entropy[1] - 1.0),
     }
+
+
+# ---------------------------------------------------- comparison baselines --
+# compare.py: the two position-wise policies the paper compares against.
+
+def position_cosines(prev_vecs, curr_vecs):
+    """Row-wise cosine, zero-norm rows score 0 (compare.py:28-38)."""
+    a = np.asarray(prev_vecs, dtype=np.float64)
+    b = np.asarray(curr_vecs, dtype=np.float64)
+    num = np.einsum("nd,nd->n", a, b)
+    den = np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1)
+    out = np.zeros(a.shape[0])
+    ok = den > 0.0
+    out[ok] = num[ok] / den[ok]
+    return out
+
+
+def patch_pixels(gray, p):
+    """Raw-pixel token stack in row-major patch order (compare.py:24-25,41-47)."""
+    rows, cols = grid_dims(gray.shape, p)
+    return gray.reshape(rows, p, cols, p).swapaxes(1, 2).reshape(rows * cols, p * p)
+
+
+def patch_amplitudes(gray, p):
+    """|fft2| of every patch, flattened (compare.py:50-52)."""
+    rows, cols = grid_dims(gray.shape, p)
+    blocks = gray.reshape(rows, p, cols, p).swapaxes(1, 2)
+    return np.abs(scipy.fft.fft2(blocks, axes=(-2, -1))).reshape(rows * cols, -1)
+
+
+def compare_cosines(prev, curr, p):
+    """(visual, naive_freq) per-patch cosines for one frame pair
+    (compare.py:90-95 with the default raw-pixel token_fn)."""
+    a, b = as_gray(prev), as_gray(curr)
+    return (position_cosines(patch_pixels(a, p), patch_pixels(b, p)),
+            position_cosines(patch_amplitudes(a, p), patch_amplitudes(b, p)))
+
+
+def latency_ms(full_ms, cached_ms, reuse_ratio, n_tokens, n_recompute):
+    """CostModel.calibrated + latency_ms (fusion.py:34-44, 47-50): affine in
+    the recomputed-token count, constants fitted in the reference's order."""
+    n_full = float(n_tokens)
+    n_cached = n_tokens * (1.0 - reuse_ratio)
+    per = (full_ms - cached_ms) / (n_full - n_cached)
+    return (full_ms - per * n_full) + per * n_recompute
+
+
+def compare_domains(frames, cfg: OracleConfig, edge_labels=None, tau_visual=0.85, tau_naive_freq=0.85,
+                    cost=(637.0, 401.0, 0.535, 196)):
+    """Three-policy comparison over consecutive pairs (compare.py:55-114)."""
+    if len(frames) < 2:
+        raise ValueError("need at least 2 frames")
+    gray = [as_gray(f) for f in frames]
+    p = int(cfg.patch_size)
+    rows, cols = grid_dims(gray[0].shape, p)
+    n = rows * cols
+    names = ("freqcache", "visual", "naive_freq")
+    reused = dict.fromkeys(names, 0)
+    false_reuse = dict.fromkeys(names, 0)
+    lat = dict.fromkeys(names, 0.0)
+    lm = lambda k: latency_ms(*cost, k)  # noqa: E731
+    for t in range(1, len(gray)):
+        d = decide(gray[t - 1], gray[t], cfg, step=t)
+        vis, nf = compare_cosines(gray[t - 1], gray[t], p)
+        sets = {"freqcache": set(d.reuse_set),
+                "visual": set(np.flatnonzero(vis > tau_visual).tolist()),
+                "naive_freq": set(np.flatnonzero(nf > tau_naive_freq).tolist())}
+        labels = frozenset(edge_labels[t]) if edge_labels is not None else frozenset()
+        for k, s in sets.items():
+            reused[k] += len(s)
+            false_reuse[k] += len(s & labels)
+            lat[k] += lm(n - len(s))
+    steps = len(gray) - 1
+    base = lm(n)
+    pol = {}
+    for k in names:
+        m = lat[k] / steps
+        pol[k] = {"reuse_ratio": reused[k] / (steps * n),
+                  "edge_false_reuse": false_reuse[k] if edge_labels is not None else None,
+                  "mean_latency_ms": m, "speedup": base / m}
+    return {"n_steps": steps, "n_tokens": n, "baseline_latency_ms": base,
+            "thresholds": {"tau_visual": tau_visual, "tau_naive_freq": tau_naive_freq},
+            "policies": pol}

@@ -43,7 +43,7 @@ EXPORTS = (
     "fc_state_reset", "fc_select", "fc_select_profile", "fc_patch_energy", "fc_splice",
     "fc_splice_map", "fc_stage_workspace_bytes", "fc_amp_cosine", "fc_spectral_sums",
     "fc_refresh_mask", "fc_topk_ascending", "fc_render_masks", "fc_splice_packed",
-    "fc_splice_inplace", "fc_splice_inplace_scratch_bytes",
+    "fc_splice_inplace", "fc_splice_inplace_scratch_bytes", "fc_compare_cosines", "fc_row_cosines",
 )
 
 
@@ -121,6 +121,8 @@ def load(path=None):
         "fc_spectral_sums": (C.c_int, [vp, i64, i32, vp, vp, vp, vp]),
         "fc_refresh_mask": (C.c_int, [vp, i64, C.c_double, vp, vp, vp, vp]),
         "fc_topk_ascending": (C.c_int, [vp, i64, vp, i64, i64, vp, vp, vp]),
+        "fc_compare_cosines": (C.c_int, [C.POINTER(Geometry), vp, vp, vp, vp, vp]),
+        "fc_row_cosines": (C.c_int, [i64, i64, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -19,6 +19,7 @@
 
 #include "fc_kernels.cuh"
 #include "fc_fast448.cuh"
+#include "fc_compare.cuh"
 #include "fc_stages.cuh"
 
 namespace {
@@ -585,6 +586,41 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
       total, n_tokens, row_bytes / 16, src_map, reinterpret_cast<int4*>(cache0), reinterpret_cast<int4*>(cache1),
       ages0, ages1, slot_in, slot_out, rows, counts, reinterpret_cast<const int4*>(fresh),
       fresh_layout == FC_FRESH_COMPACT, fresh_rows);
+  return launch_check();
+}
+
+int fc_compare_cosines(const fc_geometry* geom, const void* prev, const void* curr, double* visual_cos,
+                       double* naive_cos, void* stream) {
+  if (!geom || !prev || !curr || !visual_cos || !naive_cos) return FC_EINVAL;
+  const fc_geometry& g = *geom;
+  if (g.batch < 1 || g.height < 1 || g.width < 1 || g.patch_size < 2) return FC_EINVAL;
+  if (g.format != FC_FMT_RGB_F32 && g.format != FC_FMT_GRAY_F32 && g.format != FC_FMT_GRAY_F64) return FC_EINVAL;
+  if (g.height % g.patch_size || g.width % g.patch_size) return FC_EINVAL;
+  if (g.patch_size > 32) return FC_EUNSUPPORTED;
+  CmpGeom cg;
+  cg.B = g.batch; cg.H = g.height; cg.W = g.width; cg.P = g.patch_size; cg.fmt = g.format;
+  cg.rows = g.height / g.patch_size;
+  cg.cols = g.width / g.patch_size;
+  cg.U = g.patch_size / 2 + 1;
+  // patches per CTA: as many as fit ~96 KB, then balanced over the chunks
+  int cmax = 1;
+  while (cmax < cg.cols && compare_smem_bytes(cg.P, cmax + 1) <= 96 * 1024) ++cmax;
+  cg.nchunk = (cg.cols + cmax - 1) / cmax;
+  cg.cpp = (cg.cols + cg.nchunk - 1) / cg.nchunk;
+  const size_t smem = compare_smem_bytes(cg.P, cg.cpp);
+  if ((long long)cg.rows * cg.nchunk > 0x7fffffffLL || g.batch > 65535) return FC_EUNSUPPORTED;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_compare, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_compare<<<dim3(cg.rows * cg.nchunk, g.batch), 256, smem, as_stream(stream)>>>(cg, prev, curr, visual_cos,
+                                                                                  naive_cos);
+  return launch_check();
+}
+
+int fc_row_cosines(int64_t n, int64_t d, const double* a, const double* b, double* out, void* stream) {
+  if (n < 0 || d < 0 || (n > 0 && (!a || !b || !out))) return FC_EINVAL;
+  if (n == 0) return FC_OK;
+  const int64_t blocks = (n * 32 + 255) / 256;
+  if (blocks > 0x7fffffffLL) return FC_EUNSUPPORTED;
+  k_row_cosines<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(n, d, a, b, out);
   return launch_check();
 }
 

@@ -169,6 +169,65 @@ class FreqCacheEngine:
         return energy
 
 
+    def compare_cosines(self, prev, curr, visual=None, naive=None):
+        """Per-patch (visual, naive_freq) cosines of this engine's B frame
+        pairs (see :func:`compare_cosines`)."""
+        self._check_frames(prev)
+        self._check_frames(curr)
+        return compare_cosines(prev, curr, self.patch_size, visual, naive)
+
+
+def compare_cosines(prev, curr, patch_size, visual=None, naive=None):
+    """Per-patch (visual, naive_freq) cosines of B frame pairs — the two
+    position-wise baseline policies of compare.py:23-52 — as [B, N] float64
+    device tensors.  Frames: [B, H, W] float64 / float32 or [B, H, W, 3]
+    float32 RGB (luma adapter), contiguous on one CUDA device."""
+    lib = nat.lib()
+    if prev.shape != curr.shape or prev.dtype != curr.dtype or prev.device != curr.device:
+        raise ValueError("prev and curr must share shape, dtype and device")
+    if not (prev.is_cuda and prev.is_contiguous() and curr.is_contiguous()):
+        raise ValueError("frames must be contiguous CUDA tensors")
+    if prev.dim() == 4 and prev.shape[-1] == 3 and prev.dtype == torch.float32:
+        fmt = nat.FC_FMT_RGB_F32
+    elif prev.dim() == 3 and prev.dtype == torch.float32:
+        fmt = nat.FC_FMT_GRAY_F32
+    elif prev.dim() == 3 and prev.dtype == torch.float64:
+        fmt = nat.FC_FMT_GRAY_F64
+    else:
+        raise ValueError(f"unsupported frame layout {prev.dtype} {tuple(prev.shape)}")
+    B, H, W = (int(v) for v in prev.shape[:3])
+    p = int(patch_size)
+    if p < 2 or H % p or W % p:
+        raise ValueError(f"patch size {p} does not divide frame dimensions {H}x{W}")
+    shape = (B, (H // p) * (W // p))
+    if visual is None:
+        visual = torch.empty(shape, dtype=torch.float64, device=prev.device)
+    if naive is None:
+        naive = torch.empty(shape, dtype=torch.float64, device=prev.device)
+    geom = nat.Geometry(B, H, W, p, fmt)
+    with torch.cuda.device(prev.device):
+        rc = lib.fc_compare_cosines(C.byref(geom), _ptr(prev), _ptr(curr), _ptr(visual), _ptr(naive),
+                                    _stream(prev.device))
+    nat.check(rc, "fc_compare_cosines")
+    return visual, naive
+
+
+def row_cosines(a, b, out=None):
+    """Row-wise cosine of two [n, d] float64 device stacks (compare.py:28-38)."""
+    lib = nat.lib()
+    if a.shape != b.shape or a.dim() != 2 or a.dtype != torch.float64 or b.dtype != torch.float64:
+        raise ValueError("row_cosines needs two float64 [n, d] tensors of one shape")
+    if not (a.is_cuda and b.is_cuda and a.is_contiguous() and b.is_contiguous()):
+        raise ValueError("row_cosines operands must be contiguous CUDA tensors")
+    if out is None:
+        out = torch.empty(a.shape[0], dtype=torch.float64, device=a.device)
+    with torch.cuda.device(a.device):
+        rc = lib.fc_row_cosines(int(a.shape[0]), int(a.shape[1]), _ptr(a), _ptr(b), _ptr(out),
+                                _stream(a.device))
+    nat.check(rc, "fc_row_cosines")
+    return out
+
+
 def splice(src_map, cache, cache_ages, fresh, out, out_ages, compact=False):
     """Token splice on device (fusion.py:462-512), any element type.
 

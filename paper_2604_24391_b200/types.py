@@ -114,8 +114,11 @@ class CostModel:
 
     @classmethod
     def calibrated(cls, full_ms, cached_ms, reuse_ratio, n_tokens):
-        slope = (full_ms - cached_ms) / (n_tokens * reuse_ratio)
-        return cls(full_ms - slope * n_tokens, slope)
+        # same operation order as fusion.py:37-44 (bit-identical constants)
+        n_full = float(n_tokens)
+        n_cached = n_tokens * (1.0 - reuse_ratio)
+        per = (full_ms - cached_ms) / (n_full - n_cached)
+        return cls(full_ms - per * n_full, per)
 
 
 DEFAULT_COST_MODEL = CostModel.calibrated(637.0, 401.0, 0.535, 196)

@@ -65,3 +65,40 @@ def small_cases():
 
 C1 = dict(seed=1000, stream=0, steps=32, size=224, patch=14, alpha=(0.5, 0.5))
 C2 = dict(seed=2000, streams=2, steps=14, size=448, patch=14, refresh_shift=1)
+
+
+def compare_cases():
+    """(name, frames, cfg-dict, edge_labels | None) for compare_domains
+    (compare.py:55-114) over the shapes of test_compare.py."""
+    out = []
+    rng = np.random.default_rng(4242)
+    base = rng.random((64, 64))
+    out.append(("translate", [np.roll(base, (3 * t, 5 * t), axis=(0, 1)) for t in range(6)],
+                {"patch_size": 8}, None))
+    # persistent sharp rectangle over a smooth drifting background; labels =
+    # patches crossed by the rectangle's boundary
+    yy, xx = np.mgrid[0:96, 0:96] / 96.0
+    frames, labels = [], []
+    r0, r1, c0, c1 = 20, 61, 28, 75
+    edge = set()
+    for i in range(12):
+        for j in range(12):
+            ys, xs = set(range(8 * i, 8 * i + 8)), set(range(8 * j, 8 * j + 8))
+            on_r = bool(ys & {r0, r1 - 1}) and bool(xs & set(range(c0, c1)))
+            on_c = bool(xs & {c0, c1 - 1}) and bool(ys & set(range(r0, r1)))
+            if on_r or on_c:
+                edge.add(12 * i + j)
+    for t in range(12):
+        f = 0.25 + 0.2 * np.sin(2 * np.pi * (xx + 0.02 * t)) * np.cos(2 * np.pi * yy)
+        f = f + 0.01 * rng.standard_normal((96, 96))
+        f[r0:r1, c0:c1] = 1.0
+        frames.append(f)
+        labels.append(sorted(edge))
+    out.append(("edge", frames, {"patch_size": 8}, labels))
+    st = rng.random((64, 64))
+    out.append(("static", [st.copy() for _ in range(6)],
+                {"patch_size": 8, "edge_lambda": 1e15, "alpha_min": 0.4, "alpha_max": 0.4}, None))
+    out.append(("random", [rng.random((32, 32)) for _ in range(3)], {"patch_size": 8}, None))
+    out.append(("p14", [np.roll(rng.random((112, 112)), (t, 2 * t), axis=(0, 1)) for t in range(4)],
+                {"patch_size": 14}, None))
+    return out

@@ -30,7 +30,9 @@ sys.path.insert(0, str(HERE))
 import freqcache as ref  # noqa: E402
 from freqcache.frameio import LUMA_WEIGHTS  # noqa: E402
 
-from cases import C1, C2, fhash, small_cases  # noqa: E402
+from cases import C1, C2, compare_cases, fhash, small_cases  # noqa: E402
+from freqcache.compare import compare_domains as ref_compare  # noqa: E402
+from freqcache.compare import _patch_amplitudes, _position_cosines, _token_stack, _raw_pixels  # noqa: E402
 from paper_2604_24391_b200.synth import stream_frames  # noqa: E402
 
 
@@ -110,6 +112,20 @@ def main():
     (HERE / "golden_step.json").write_text(json.dumps({
         "frames": [fhash(f) for f in frames], "steps": steps,
         "sequence_seed": 77, "sequence_mean_reuse": seq.mean_reuse_ratio, "sequence_speedup": seq.speedup}))
+    # compare_domains reports (compare.py:55-114) + the BASELINE-geometry
+    # per-patch cosines of one RGB pair (gray via the reference luma weights)
+    cmp = []
+    for name, frs, c, labels in compare_cases():
+        rep = ref_compare(frs, cfg_of(c), edge_labels=labels)
+        cmp.append({"name": name, "cfg": c, "frames": [fhash(f) for f in frs], "report": rep})
+    fr = stream_frames(C2["seed"], 0, 2, C2["size"], C2["size"])
+    g0, g1 = ref_gray(fr[0]), ref_gray(fr[1])
+    grid = ref.PatchGrid(g0, C2["patch"])
+    vis = _position_cosines(_token_stack(grid, g0, _raw_pixels), _token_stack(grid, g1, _raw_pixels))
+    nf = _position_cosines(_patch_amplitudes(grid, g0), _patch_amplitudes(grid, g1))
+    (HERE / "golden_compare.json").write_text(json.dumps({
+        "cases": cmp, "pair": {"recipe": C2, "frames": [fhash(f) for f in fr],
+                               "visual": vis.tolist(), "naive_freq": nf.tolist()}}))
     print("wrote fixtures:", [p.name for p in HERE.glob("golden_*.json")])
 
 

@@ -176,3 +176,43 @@ def test_white_noise_regression_anchor():
     ks = [O.decide(frames[t - 1], frames[t], cfg).k_final for t in range(1, 8)]
     assert sum(ks) / (7 * 64) == pytest.approx(0.3392857142857143, abs=1e-12)
     assert gold["sequence_mean_reuse"] > 0
+
+
+# ------------------------------------------- comparison baselines (§8f #3) --
+
+def _report_same(rep, gold, ftol=1e-12):
+    assert rep["n_steps"] == gold["n_steps"] and rep["n_tokens"] == gold["n_tokens"]
+    assert rep["thresholds"] == gold["thresholds"]
+    assert math.isclose(rep["baseline_latency_ms"], gold["baseline_latency_ms"], rel_tol=ftol)
+    for name, g in gold["policies"].items():
+        r = rep["policies"][name]
+        assert r["reuse_ratio"] == g["reuse_ratio"], name
+        assert r["edge_false_reuse"] == g["edge_false_reuse"], name
+        assert math.isclose(r["mean_latency_ms"], g["mean_latency_ms"], rel_tol=ftol), name
+        assert math.isclose(r["speedup"], g["speedup"], rel_tol=ftol), name
+
+
+def test_oracle_compare_domains_matches_reference():
+    from cases import compare_cases
+    gold = {c["name"]: c for c in json.loads((GOLD / "golden_compare.json").read_text())["cases"]}
+    for name, frames, c, labels in compare_cases():
+        g = gold[name]
+        assert [fhash(f) for f in frames] == g["frames"], name
+        _report_same(O.compare_domains(frames, _ocfg(c), edge_labels=labels), g["report"])
+
+
+def test_oracle_compare_cosines_baseline_pair():
+    from paper_2604_24391_b200.synth import stream_frames
+    pair = json.loads((GOLD / "golden_compare.json").read_text())["pair"]
+    r = pair["recipe"]
+    fr = stream_frames(r["seed"], 0, 2, r["size"], r["size"])
+    assert [fhash(f) for f in fr] == pair["frames"]
+    vis, nf = O.compare_cosines(fr[0], fr[1], r["patch"])
+    np.testing.assert_allclose(vis, pair["visual"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(nf, pair["naive_freq"], rtol=1e-12, atol=1e-14)
+
+
+def test_oracle_position_cosines_zero_norm():
+    a = np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 1.0]])
+    b = np.array([[1.0, 1.0], [0.0, 1.0], [2.0, 2.0]])
+    np.testing.assert_allclose(O.position_cosines(a, b), [0.0, 0.0, 1.0])
