@@ -55,6 +55,10 @@ extern "C" {
 #define FC_FMT_RGB_F32   0  /* [B][H][W][3] float32, BT.601 luma in fp64     */
 #define FC_FMT_GRAY_F32  1  /* [B][H][W]    float32                          */
 #define FC_FMT_GRAY_F64  2  /* [B][H][W]    float64 (the reference's frames) */
+#define FC_FMT_GRAY_U8   3  /* [B][H][W]    uint8, gray = v / 255 (PGM P5,
+                               frameio.py:81-88)                           */
+#define FC_FMT_RGB_U8    4  /* [B][H][W][3] uint8, gray = luma(v) / 255 in
+                               fp64 (PPM P6, frameio.py:81-88)              */
 
 /* fresh-row layouts for fc_splice */
 #define FC_FRESH_DENSE    0  /* fresh row of token p is fresh[b][p]          */

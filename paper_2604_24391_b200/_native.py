@@ -33,6 +33,8 @@ DIAG_TEXT = {
 FC_FMT_RGB_F32 = 0
 FC_FMT_GRAY_F32 = 1
 FC_FMT_GRAY_F64 = 2
+FC_FMT_GRAY_U8 = 3
+FC_FMT_RGB_U8 = 4
 
 FC_FRESH_DENSE = 0
 FC_FRESH_COMPACT = 1

@@ -110,6 +110,8 @@ void* sel_rows_inv(int k) { return k == 448 ? ptr_rows_inv<448>() : k == 224 ? p
 void* sel_fast_rows_fwd(int fmt) {
   return fmt == FC_FMT_RGB_F32 ? (void*)k448_rows_fwd<FC_FMT_RGB_F32>
        : fmt == FC_FMT_GRAY_F32 ? (void*)k448_rows_fwd<FC_FMT_GRAY_F32>
+       : fmt == FC_FMT_GRAY_U8 ? (void*)k448_rows_fwd<FC_FMT_GRAY_U8>
+       : fmt == FC_FMT_RGB_U8 ? (void*)k448_rows_fwd<FC_FMT_RGB_U8>
                                 : (void*)k448_rows_fwd<FC_FMT_GRAY_F64>;
 }
 
@@ -260,7 +262,7 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
   if (g.batch < 1 || g.height < 1 || g.width < 1) return FC_EINVAL;
   if (g.patch_size < 2) return FC_EINVAL;                                  // frame.py:31-32
   if (g.height % g.patch_size || g.width % g.patch_size) return FC_EINVAL; // frame.py:33-37
-  if (g.format < FC_FMT_RGB_F32 || g.format > FC_FMT_GRAY_F64) return FC_EINVAL;
+  if (g.format < FC_FMT_RGB_F32 || g.format > FC_FMT_RGB_U8) return FC_EINVAL;
   const int P = g.patch_size, H = g.height, W = g.width;
   const int rows = H / P, cols = W / P, N = rows * cols;
   if (P > FC_MAX_PATCH || N > FC_MAX_TOKENS || H > 1536 || W > 1536) return FC_EUNSUPPORTED;
@@ -594,7 +596,7 @@ int fc_compare_cosines(const fc_geometry* geom, const void* prev, const void* cu
   if (!geom || !prev || !curr || !visual_cos || !naive_cos) return FC_EINVAL;
   const fc_geometry& g = *geom;
   if (g.batch < 1 || g.height < 1 || g.width < 1 || g.patch_size < 2) return FC_EINVAL;
-  if (g.format != FC_FMT_RGB_F32 && g.format != FC_FMT_GRAY_F32 && g.format != FC_FMT_GRAY_F64) return FC_EINVAL;
+  if (g.format < FC_FMT_RGB_F32 || g.format > FC_FMT_RGB_U8) return FC_EINVAL;
   if (g.height % g.patch_size || g.width % g.patch_size) return FC_EINVAL;
   if (g.patch_size > 32) return FC_EUNSUPPORTED;
   CmpGeom cg;

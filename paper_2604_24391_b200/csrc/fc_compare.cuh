@@ -38,16 +38,6 @@ inline size_t compare_smem_bytes(int P, int cpp) {
   return b;
 }
 
-__device__ __forceinline__ double cmp_gray(const void* f, int fmt, size_t i) {
-  if (fmt == FC_FMT_RGB_F32) {
-    const float* p = reinterpret_cast<const float*>(f) + 3 * i;
-    return luma_f64(p[0], p[1], p[2]);
-  } else if (fmt == FC_FMT_GRAY_F32) {
-    return (double)reinterpret_cast<const float*>(f)[i];
-  }
-  return reinterpret_cast<const double*>(f)[i];
-}
-
 __global__ void __launch_bounds__(256) k_compare(CmpGeom g, const void* __restrict__ prev,
                                                  const void* __restrict__ curr, double* __restrict__ vis_out,
                                                  double* __restrict__ nf_out) {
@@ -74,7 +64,7 @@ __global__ void __launch_bounds__(256) k_compare(CmpGeom g, const void* __restri
   for (int i = t; i < 2 * P * cw; i += nt) {
     const int f = i / (P * cw), rem = i - f * (P * cw), y = rem / cw, x = rem - y * cw;
     const size_t pix = fbase + (size_t)(pr * P + y) * g.W + (size_t)q0 * P + x;
-    gy[(f * P + y) * (cpp0 * P) + x] = cmp_gray(f ? curr : prev, g.fmt, pix);
+    gy[(f * P + y) * (cpp0 * P) + x] = load_gray(f ? curr : prev, g.fmt, pix);
   }
   __syncthreads();
   // ---- visual partials per (patch, row) and DFT stage 1 per (frame, patch, u, x)

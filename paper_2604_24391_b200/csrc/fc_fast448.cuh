@@ -179,6 +179,10 @@ __device__ __forceinline__ double smem_luma(const unsigned char* px, int i) {
     return luma_f64(f[0], f[1], f[2]);
   } else if constexpr (FMT == FC_FMT_GRAY_F32) {
     return (double)reinterpret_cast<const float*>(px)[i];
+  } else if constexpr (FMT == FC_FMT_GRAY_U8) {
+    return gray_u8(px[i]);
+  } else if constexpr (FMT == FC_FMT_RGB_U8) {
+    return luma_u8(px[3 * i], px[3 * i + 1], px[3 * i + 2]);
   } else {
     return reinterpret_cast<const double*>(px)[i];
   }
@@ -189,7 +193,8 @@ __global__ void __launch_bounds__(448, 3) k448_rows_fwd(KParams kp, Dct14 dc, co
                                                        int b0, int do_fft) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[2];
-  constexpr int bpp = FMT == FC_FMT_RGB_F32 ? 12 : (FMT == FC_FMT_GRAY_F32 ? 4 : 8);
+  constexpr int bpp = FMT == FC_FMT_RGB_F32 ? 12 : FMT == FC_FMT_GRAY_F32 ? 4 : FMT == FC_FMT_GRAY_U8 ? 1
+                    : FMT == FC_FMT_RGB_U8 ? 3 : 8;
   const int s = blockIdx.x, bl = blockIdx.y, b = b0 + bl;
   const int t = threadIdx.x;
   // one 73.5 KB region: the staged stripe, then (after every pixel is read)

@@ -84,6 +84,31 @@ __device__ __forceinline__ double luma_f64(float r, float g, float b) {
                    __dmul_rn(0.114, (double)b));
 }
 
+// 8-bit netpbm pixels -> the reference's gray values: v / 255 (P5) and
+// ((0.299 R + 0.587 G) + 0.114 B) / 255 (P6), fp64, correctly rounded
+// (frameio.py:81-88).
+__device__ __forceinline__ double gray_u8(unsigned v) { return __ddiv_rn((double)v, 255.0); }
+__device__ __forceinline__ double luma_u8(unsigned r, unsigned g, unsigned b) {
+  return __ddiv_rn(luma_f64((float)r, (float)g, (float)b), 255.0);
+}
+
+// Gray value of pixel i of a frame in any FC_FMT_* layout.
+__device__ __forceinline__ double load_gray(const void* f, int fmt, size_t i) {
+  switch (fmt) {
+    case FC_FMT_RGB_F32: {
+      const float* p = reinterpret_cast<const float*>(f) + 3 * i;
+      return luma_f64(p[0], p[1], p[2]);
+    }
+    case FC_FMT_GRAY_F32: return (double)reinterpret_cast<const float*>(f)[i];
+    case FC_FMT_GRAY_U8: return gray_u8(reinterpret_cast<const uint8_t*>(f)[i]);
+    case FC_FMT_RGB_U8: {
+      const uint8_t* p = reinterpret_cast<const uint8_t*>(f) + 3 * i;
+      return luma_u8(p[0], p[1], p[2]);
+    }
+    default: return reinterpret_cast<const double*>(f)[i];
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -238,6 +263,12 @@ __global__ void __launch_bounds__(FC_THREADS) k_rows_fwd(KParams kp, const void*
         mn = fmin(mn, v); mx = fmax(mx, v);
         if (!isfinite(v)) bad = 1.0;
       }
+    }
+  } else if (kp.fmt == FC_FMT_GRAY_U8 || kp.fmt == FC_FMT_RGB_U8) {
+    for (int px = threadIdx.x; px < npx; px += blockDim.x) {
+      const double v = load_gray(frames, kp.fmt, base + px);
+      g[px] = v;
+      mn = fmin(mn, v); mx = fmax(mx, v);
     }
   } else if (kp.fmt == FC_FMT_GRAY_F32) {
     const float* f = reinterpret_cast<const float*>(frames) + base;

@@ -23,6 +23,8 @@ _FORMATS = {
     "rgb": (nat.FC_FMT_RGB_F32, torch.float32, 3),
     "gray32": (nat.FC_FMT_GRAY_F32, torch.float32, 1),
     "gray64": (nat.FC_FMT_GRAY_F64, torch.float64, 1),
+    "gray_u8": (nat.FC_FMT_GRAY_U8, torch.uint8, 1),   # PGM P5 payload, gray = v / 255
+    "rgb_u8": (nat.FC_FMT_RGB_U8, torch.uint8, 3),     # PPM P6 payload, gray = luma / 255
 }
 
 
@@ -193,6 +195,10 @@ def compare_cosines(prev, curr, patch_size, visual=None, naive=None):
         fmt = nat.FC_FMT_GRAY_F32
     elif prev.dim() == 3 and prev.dtype == torch.float64:
         fmt = nat.FC_FMT_GRAY_F64
+    elif prev.dim() == 3 and prev.dtype == torch.uint8:
+        fmt = nat.FC_FMT_GRAY_U8
+    elif prev.dim() == 4 and prev.shape[-1] == 3 and prev.dtype == torch.uint8:
+        fmt = nat.FC_FMT_RGB_U8
     else:
         raise ValueError(f"unsupported frame layout {prev.dtype} {tuple(prev.shape)}")
     B, H, W = (int(v) for v in prev.shape[:3])

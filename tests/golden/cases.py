@@ -102,3 +102,35 @@ def compare_cases():
     out.append(("p14", [np.roll(rng.random((112, 112)), (t, 2 * t), axis=(0, 1)) for t in range(4)],
                 {"patch_size": 14}, None))
     return out
+
+
+def frameio_cases():
+    """(name, suffix, file bytes) for the netpbm / rawf32 readers
+    (frameio.py:29-175): valid files and every parse-failure branch."""
+    import struct
+    rng = np.random.default_rng(99)
+    out = []
+    out.append(("p5_small", ".pgm", b"P5\n2 2\n255\n" + bytes([0, 255, 128, 64])))
+    out.append(("p5_comments", ".pgm", b"P5\n# made by hand\n3 2\n# maxval next\n255\n" + bytes(range(10, 16))))
+    out.append(("p6_rand", ".ppm", b"P6 5 4 255\n" + rng.integers(0, 256, 60, dtype=np.uint8).tobytes()))
+    out.append(("p5_extra_payload", ".pgm", b"P5\n2 1\n255\n" + bytes([7, 9, 11, 13])))
+    out.append(("p5_truncated", ".pgm", b"P5\n4 4\n255\n" + bytes(10)))
+    out.append(("bad_magic", ".pgm", b"P7\n2 2\n255\n" + bytes(4)))
+    out.append(("short", ".pgm", b"P"))
+    out.append(("trunc_header", ".pgm", b"P5\n3 "))
+    out.append(("zero_dims", ".pgm", b"P5\n0 2\n255\n"))
+    out.append(("maxval16", ".pgm", b"P5\n2 2\n65535\n" + bytes(8)))
+    out.append(("non_numeric", ".pgm", b"P5\nab 2\n255\n" + bytes(4)))
+    out.append(("no_pixels", ".pgm", b"P5\n2 2\n255"))
+    fr = rng.random((2, 3, 4)).astype("<f4")
+    head = b"FQC1" + struct.pack("<III", 3, 4, 2)
+    out.append(("raw_ok", ".raw", head + fr.tobytes()))
+    out.append(("raw_magic", ".raw", b"FQC2" + head[4:] + fr.tobytes()))
+    out.append(("raw_short", ".raw", head[:10]))
+    out.append(("raw_zero", ".raw", b"FQC1" + struct.pack("<III", 0, 4, 2)))
+    out.append(("raw_trunc", ".raw", head + fr.tobytes()[:-5]))
+    out.append(("raw_trailing", ".raw", head + fr.tobytes() + b"\x00"))
+    bad = fr.copy()
+    bad[1, 2, 3] = np.inf
+    out.append(("raw_nonfinite", ".raw", head + bad.tobytes()))
+    return out

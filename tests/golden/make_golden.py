@@ -30,7 +30,7 @@ sys.path.insert(0, str(HERE))
 import freqcache as ref  # noqa: E402
 from freqcache.frameio import LUMA_WEIGHTS  # noqa: E402
 
-from cases import C1, C2, compare_cases, fhash, small_cases  # noqa: E402
+from cases import C1, C2, compare_cases, fhash, frameio_cases, small_cases  # noqa: E402
 from freqcache.compare import compare_domains as ref_compare  # noqa: E402
 from freqcache.compare import _patch_amplitudes, _position_cosines, _token_stack, _raw_pixels  # noqa: E402
 from paper_2604_24391_b200.synth import stream_frames  # noqa: E402
@@ -126,6 +126,21 @@ def main():
     (HERE / "golden_compare.json").write_text(json.dumps({
         "cases": cmp, "pair": {"recipe": C2, "frames": [fhash(f) for f in fr],
                                "visual": vis.tolist(), "naive_freq": nf.tolist()}}))
+    # frame readers (frameio.py:29-175): outputs or (message, offset)
+    import tempfile
+    from freqcache.frameio import load_frames
+    fio = []
+    with tempfile.TemporaryDirectory() as td:
+        for name, suffix, data in frameio_cases():
+            p = Path(td) / f"{name}{suffix}"
+            p.write_bytes(data)
+            try:
+                frs = load_frames(p)
+                fio.append({"name": name, "frames": [fhash(f) for f in frs], "shape": list(frs[0].shape)})
+            except Exception as e:  # noqa: BLE001
+                fio.append({"name": name, "error": type(e).__name__,
+                            "message": str(e).replace(str(p), "<path>"), "offset": getattr(e, "offset", None)})
+    (HERE / "golden_frameio.json").write_text(json.dumps(fio, indent=0))
     print("wrote fixtures:", [p.name for p in HERE.glob("golden_*.json")])
 
 
