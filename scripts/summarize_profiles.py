@@ -22,7 +22,8 @@ ROOT = Path(__file__).resolve().parent.parent
 OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
 NAMES = {"k448_rows_fwd": "rows_fwd", "k448_cols": "cols", "k448_rows_inv": "rows_inv",
-         "k_select": "select", "k_splice16": "splice"}
+         "k_select": "select", "k_splice16": "splice", "k_splice_ip": "splice", "k_splice_ip_bulk": "splice",
+         "k_splice_plan": "splice_plan"}
 
 
 def short(name):
@@ -84,9 +85,11 @@ def main(tag):
         k = short(g(d, "Kernel Name"))
         rdb = float(g(d, "dram__bytes_read.sum") or 0)
         wrb = float(g(d, "dram__bytes_write.sum") or 0)
-        unit_r = rr[1][rh.index("dram__bytes_read.sum")]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
-        traffic[k] = (rdb + wrb) * scale
+        units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rdb *= units.get(rr[1][rh.index("dram__bytes_read.sum")], 1)
+        wrb *= units.get(rr[1][rh.index("dram__bytes_write.sum")], 1)
+        scale = 1
+        traffic.setdefault(k, []).append(rdb + wrb)
         st = sorted(((h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""),
                       float(g(d, h) or 0)) for h in stalls), key=lambda x: -x[1])[:3]
         tu = rr[1][rh.index("gpu__time_duration.sum")]
@@ -101,6 +104,11 @@ def main(tag):
     for k, v in bench["kernels"].items():
         lines.append(f"| {k} | {v['ms']:.3f} | {100 * v['share']:.1f} % | {v['bytes'] / 1e6:.0f} MB | {v['gbs']:.0f} |")
     (PROF / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
+    # per-launch DRAM bytes (mean over the captured launches); the bench's
+    # "splice" timing covers the plan kernel and the copy kernel together
+    traffic = {k: sum(v) / len(v) for k, v in traffic.items()}
+    if "splice_plan" in traffic and "splice" in traffic:
+        traffic["splice"] += traffic.pop("splice_plan")
     (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1))
     print("\n".join(lines))
 
