@@ -18,7 +18,7 @@
 #include <vector>
 
 #include "fc_kernels.cuh"
-#include "fc_fast448.cuh"
+#include "fc_fast448w.cuh"
 #include "fc_compare.cuh"
 #include "fc_stages.cuh"
 
@@ -46,8 +46,6 @@ struct fc_plan {
   cudaEvent_t fork = nullptr;
   cudaEvent_t join[kMaxLanes] = {};
   size_t lane_stride = 0;              // workspace bytes per lane (T1 + T2)
-  bool persistent = false;             // fast path: persistent K_B / K_C (FC_PERSISTENT=1)
-  int gridB = 0, gridC = 0;            // persistent grid sizes (SMs x occupancy)
   void* fnB = nullptr;                 // K_B / K_C variants (occupancy x twiddle mode)
   void* fnC = nullptr;
   float2* d_twW = nullptr;
@@ -197,21 +195,11 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
       fa<<<dim3(32, nb), 448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1);
       if (rec) rec->mark(st, 0);
-      if (pl->persistent) {
-        const int gb = nb * kNCB448 < pl->gridB ? nb * kNCB448 : pl->gridB;
-        k448_cols_p<<<gb, 64 * kBC, kSmemBP, ls>>>(kl, b0, nb);
-      } else {
-        auto fb = (void (*)(KParams, int))pl->fnB;
-        fb<<<dim3(kNCB448, nb), 64 * kBC, pl->smemB, ls>>>(kl, b0);
-      }
+      auto fb = (void (*)(KParams, int))pl->fnB;
+      fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0);
       if (rec) rec->mark(st, 1);
-      if (pl->persistent) {
-        const int gc = nb * kNRG448 < pl->gridC ? nb * kNRG448 : pl->gridC;
-        k448_rows_inv_p<<<gc, 64 * kBP, kSmemCP, ls>>>(kl, b0, nb);
-      } else {
-        auto fc = (void (*)(KParams, int))pl->fnC;
-        fc<<<dim3(kNRG448, nb), 64 * kBP, pl->smemC, ls>>>(kl, b0);
-      }
+      auto fc = (void (*)(KParams, int))pl->fnC;
+      fc<<<dim3(kNRG448, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
       if (rec) rec->mark(st, 2);
     }
     if (!rec) {
@@ -298,8 +286,8 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     pl->lanes = env_int("FC_LANES", kLanesDefault, 1, kMaxLanes);
     if (pl->lanes > nchunks) pl->lanes = nchunks;
     pl->smemA = (size_t)kPxBytes448;
-    pl->smemB = (size_t)kScratchB + kStBlock + (size_t)2 * 448 * sizeof(float2);
-    pl->smemC = (size_t)(kBP * f448::XR) * sizeof(float2);
+    pl->smemB = (size_t)kSmemB448;
+    pl->smemC = (size_t)kSmemC448;
     kp.NCB = kNCB448;   // K_B stats partials per stream
     kp.NRG = kNRG448;   // K_C peak partials per stream
     const size_t ch = pl->chunk;
@@ -309,7 +297,7 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     pl->off_T = off;
     pl->off_T2 = off + t1;
     off += pl->lane_stride * pl->lanes;
-    specElems = B * kNCB448 * 64 * kBC * 8;  // register-order state
+    specElems = B * 224 * kStCol * 2;  // register-order state (float2 count)
   } else {
     pl->chunk = g.batch;
     const int maxpairC = (kp.RG + 1) / 2;
@@ -372,26 +360,14 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     if (pl->fast) {
       rc = set_smem(sel_fast_rows_fwd(g.format), pl->smemA);
       // occupancy variants: FC_OCC_B / FC_OCC_C = target CTAs per SM (register
-      // cap), twiddles read at use when the cap is tight
-      const int ob = env_int("FC_OCC_B", 3, 3, 6), oc = env_int("FC_OCC_C", 6, 3, 6);
-      pl->fnB = ob == 6 ? (void*)k448_cols<6, true> : ob == 5 ? (void*)k448_cols<5, true>
-              : ob == 3 ? (void*)k448_cols<4, true> : (void*)k448_cols<4, false>;
-      pl->fnC = oc == 6 ? (void*)k448_rows_inv<6, true> : oc == 5 ? (void*)k448_rows_inv<5, true>
-              : oc == 3 ? (void*)k448_rows_inv<4, true> : (void*)k448_rows_inv<4, false>;
+      // cap); twiddles are read at use (lazy) when the cap is tight
+      const int ob = env_int("FC_OCC_B", 6, 4, 8), oc = env_int("FC_OCC_C", 7, 4, 10);
+      pl->fnB = ob >= 6 ? (void*)k448_cols<6, true> : ob == 5 ? (void*)k448_cols<5, false>
+              : (void*)k448_cols<4, false>;
+      pl->fnC = oc >= 10 ? (void*)k448_rows_inv<10, true> : oc >= 8 ? (void*)k448_rows_inv<8, true>
+              : oc == 7 ? (void*)k448_rows_inv<7, true> : (void*)k448_rows_inv<6, false>;
       if (rc == FC_OK) rc = set_smem(pl->fnB, pl->smemB);
       if (rc == FC_OK) rc = set_smem(pl->fnC, pl->smemC);
-      if (rc == FC_OK) rc = set_smem((void*)k448_cols_p, kSmemBP);
-      if (rc == FC_OK) rc = set_smem((void*)k448_rows_inv_p, kSmemCP);
-      if (rc == FC_OK) {
-        int dev = 0, sms = 148, ob = 0, oc = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k448_cols_p, 64 * kBC, kSmemBP);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k448_rows_inv_p, 64 * kBP, kSmemCP);
-        pl->gridB = sms * (ob > 0 ? ob : 1);
-        pl->gridC = sms * (oc > 0 ? oc : 1);
-        pl->persistent = env_int("FC_PERSISTENT", 0, 0, 1) != 0;
-      }
     } else {
       rc = set_smem(sel_rows_fwd(pl->kw), pl->smemA);
       if (rc == FC_OK) rc = set_smem(sel_cols(pl->kh), pl->smemB);

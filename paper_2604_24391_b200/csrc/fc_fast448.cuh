@@ -165,12 +165,11 @@ struct Dct14 {
 //          (fp64), fp32 gray pairs for the FFT;
 // phase 2: E = sum s2 - sum_{u,v<3} (sum_y T[u][y] C[v][y])^2 per patch;
 // phase 3: 7 packed-pair forward FFTs (row pairs as complex);
-// phase 4: split pairs, write packed half-spectrum columns to T1.
+// phase 4: split pairs, write packed half-spectrum columns to T1, which is
+//          column-major ([stream][q][448 rows] complex64): K_B stages one
+//          contiguous 3.5 KB column per warp.
 constexpr int kPxBytes448 = 14 * 448 * 12;  // largest stripe (fp32 RGB)
-constexpr int kBC = 4;                       // packed columns per K_B CTA
-constexpr int kNCB448 = 224 / kBC;           // column blocks
-constexpr int kBP = 4;                       // row pairs per K_C CTA
-constexpr int kNRG448 = 448 / (2 * kBP);     // row groups
+static_assert(448 * 9 * 8 <= 7 * 448 * 8 + (4 * 480 + 288) * 8, "zout must not reach the FFT scratch");
 
 template <int FMT>
 __device__ __forceinline__ double smem_luma(const unsigned char* px, int i) {
@@ -295,520 +294,33 @@ __global__ void __launch_bounds__(448, 3) k448_rows_fwd(KParams kp, Dct14 dc, co
   for (int n1 = 0; n1 < 7; ++n1) a[n1] = zin[g * 448 + 64 * n1 + r];
   const f448::TwLazy tw{kp.tw448, kp.tw64, r};
   f448::fwd<false>(a, bv, S + g * f448::XR, r, tw);
-  float2* zout = zin;  // zin fully consumed before fwd's first barrier
+  // zout[k][9]: bin k of pair g at k * 9 + g (zin and part are consumed; S
+  // may still be read by other transforms, zout does not overlap it)
+  float2* zout = zin;
   if (r < 56) {
     const int k1 = r >> 3, j1 = r & 7;
 #pragma unroll
-    for (int j2 = 0; j2 < 8; ++j2) zout[g * 448 + k1 + 7 * j1 + 56 * j2] = bv[j2];
+    for (int j2 = 0; j2 < 8; ++j2) zout[(k1 + 7 * j1 + 56 * j2) * 9 + g] = bv[j2];
   }
   __syncthreads();
 
-  // ---- phase 4: split the two real rows' spectra, write packed columns
+  // ---- phase 4: split the two real rows' spectra; consecutive threads take
+  // consecutive row pairs of one column, so each column's 14 stripe rows
+  // (112 contiguous bytes of T1) are written by neighbouring lanes
   for (int idx = t; idx < 7 * 224; idx += 448) {
-    const int gg = idx / 224, q = idx - (idx / 224) * 224;
-    const float2* Z = zout + gg * 448;
+    const int q = idx / 7, gg = idx - (idx / 7) * 7;
     float2 xa, xb;
     if (q == 0) {
-      const float2 z0 = Z[0], zn = Z[224];
+      const float2 z0 = zout[gg], zn = zout[224 * 9 + gg];
       xa = make_float2(z0.x, zn.x);
       xb = make_float2(z0.y, zn.y);
     } else {
-      const float2 za = Z[q], zm = Z[448 - q];
+      const float2 za = zout[q * 9 + gg], zm = zout[(448 - q) * 9 + gg];
       xa = make_float2(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y));
       xb = make_float2(0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
     }
     const int ra = s * 14 + 2 * gg;
-    float2* dst = kp.T + (((size_t)bl * kNCB448 + q / kBC) * 448 + ra) * kBC + (q % kBC);
-    dst[0] = xa;
-    dst[kBC] = xb;
+    *reinterpret_cast<float4*>(kp.T + ((size_t)bl * 224 + q) * 448 + ra) = make_float4(xa.x, xa.y, xb.x, xb.y);
   }
 }
 
-// ------------------------------------------------------------- K_B 448 ----
-// One CTA per (kBC-column block, stream); 64*kBC threads, column c = t % kBC
-// fastest.  The T1 block and the stream's previous spectrum are staged by
-// two TMA bulk copies at kernel start.  State layout is the register order
-// of the forward column FFT: spec[b][cb][i][t] float4 (j2 = 2i, 2i+1), so
-// the state swap is coalesced and its shared-memory reads conflict-free.
-constexpr int kT1Block = 448 * kBC * 8;      // bytes
-constexpr int kStBlock = 64 * kBC * 8 * 8;   // bytes
-constexpr int kXCB = 516;                    // scratch stride, 4 interleaved transforms
-constexpr int kScratchB = kBC * kXCB * 8;
-
-template <int MINB, bool LAZY>
-__global__ void __launch_bounds__(64 * kBC, MINB) k448_cols(KParams kp, int b0) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ double red[16 * 4];
-  const int cb = blockIdx.x, bl = blockIdx.y, b = b0 + bl;
-  const int t = threadIdx.x;
-  const int c = t % kBC, r = t / kBC;
-  float2* t1 = reinterpret_cast<float2*>(smem);                   // T1 block, then scratch
-  float2* S = reinterpret_cast<float2*>(smem) + c * kXCB;         // [kBC][516] (aliases t1)
-  float2* prev = reinterpret_cast<float2*>(smem + kScratchB);     // [64 kBC][8]
-  float2* col0 = prev + 64 * kBC * 8;                             // [2][448] (cb == 0)
-  const bool valid = kp.hdr[b].valid != 0;
-  float2* stg = kp.spec + (((size_t)b * kNCB448 + cb) * 64 * kBC) * 8;
-  if (t == 0) {
-    tma::bar_init(&bar[0], 1);
-    tma::bar_init(&bar[1], 1);
-  }
-  __syncthreads();
-  if (t == 0) {
-    tma::load_tile(t1, kp.T + ((size_t)bl * kNCB448 + cb) * 448 * kBC, kT1Block, &bar[0]);
-    if (valid) tma::load_tile(prev, stg, kStBlock, &bar[1]);
-  }
-  const auto tw = TwSel<LAZY>::make(kp, r);
-  tma::bar_wait(&bar[0], 0);
-  float2 a[7], v[8];
-#pragma unroll
-  for (int n1 = 0; n1 < 7; ++n1) a[n1] = t1[64 * kBC * n1 + t];
-  __syncthreads();  // t1 consumed: scratch may overwrite it
-  f448::fwd<false>(a, v, S, r, tw);
-
-  const bool act = r < 56;
-  const int k1 = r >> 3, j1 = r & 7;
-  float4* st = reinterpret_cast<float4*>(stg) + t;  // chunk i at st[i * 64 * kBC]
-  // the previous spectrum must have landed before this block is overwritten
-  if (valid) tma::bar_wait(&bar[1], 0);
-  __syncthreads();
-  if (act) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) st[i * 64 * kBC] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
-  }
-  if (!valid) return;  // cold stream: spectrum established (block-uniform)
-  float2 p[8];
-  if (act) {
-    const float4* pv = reinterpret_cast<const float4*>(prev) + t;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 q = pv[i * 64 * kBC];
-      p[2 * i] = make_float2(q.x, q.y);
-      p[2 * i + 1] = make_float2(q.z, q.w);
-    }
-  }
-  float spc = 0.f, spp = 0.f, scc = 0.f, splp = 0.f;
-  auto acc = [&](float w, float2 fp, float2 fc) -> float2 {
-    const float pp = fp.x * fp.x + fp.y * fp.y;
-    const float pc = fc.x * fc.x + fc.y * fc.y;
-    const float m = sqrt_approx(pp * pc);  // |Fp| |Fc|
-    spc = fmaf(w, m, spc);
-    spp = fmaf(w, pp, spp);
-    scc = fmaf(w, pc, scc);
-    if (pc > 0.f) splp = fmaf(w * pc, __logf(pc), splp);
-    // normalised cross-power (migration.py:130-131)
-    const float inv = rcp_approx(m + 1e-12f);
-    return make_float2((fp.x * fc.x + fp.y * fc.y) * inv, (fp.y * fc.x - fp.x * fc.y) * inv);
-  };
-  if (cb == 0) {
-    // packed DC/Nyquist column: needs bins k and 448-k of both spectra
-    if (c == 0 && act) {
-#pragma unroll
-      for (int j2 = 0; j2 < 8; ++j2) {
-        const int k = k1 + 7 * j1 + 56 * j2;
-        col0[k] = v[j2];
-        col0[448 + k] = p[j2];
-      }
-    }
-    __syncthreads();
-    if (c == 0 && act) {
-#pragma unroll
-      for (int j2 = 0; j2 < 8; ++j2) {
-        const int k = k1 + 7 * j1 + 56 * j2;
-        const int km = (448 - k) % 448;
-        float2 c0, cn, p0, pn;
-        unpack_dcny(v[j2], col0[km], c0, cn);
-        unpack_dcny(p[j2], col0[448 + km], p0, pn);
-        const float2 x0 = acc(1.f, p0, c0);
-        const float2 xn = acc(1.f, pn, cn);
-        v[j2] = make_float2(x0.x - xn.y, x0.y + xn.x);
-      }
-    }
-  }
-  if (act && !(cb == 0 && c == 0)) {
-#pragma unroll
-    for (int j2 = 0; j2 < 8; ++j2) v[j2] = acc(2.f, p[j2], v[j2]);
-  }
-  f448::inv<true>(v, a, S, r, tw);
-  float2* T2 = kp.T2 + (size_t)bl * 448 * 224 + cb * kBC + c;
-#pragma unroll
-  for (int n1 = 0; n1 < 7; ++n1) T2[(size_t)(64 * n1 + r) * 224] = a[n1];
-
-  const float fs[4] = {spc, spp, scc, splp};
-  double sums[4];
-  block_sum_f2d<4>(fs, sums, red);
-  if (t == 0) {
-    double* o = kp.stats + ((size_t)b * kNCB448 + cb) * 4;
-    o[0] = sums[0]; o[1] = sums[1]; o[2] = sums[2]; o[3] = sums[3];
-  }
-}
-
-// ------------------------------------------------------------- K_C 448 ----
-// One CTA per (2 kBP rows, stream); 64*kBP threads = kBP row pairs x 64 roles.
-// The rows of T2 (contiguous) arrive by one TMA bulk copy.
-constexpr int kT2Rows = 2 * kBP * 224 * 8;  // bytes
-
-template <int MINB, bool LAZY>
-__global__ void __launch_bounds__(64 * kBP, MINB) k448_rows_inv(KParams kp, int b0) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ PeakKey redk[16];
-  __shared__ float redv[16];
-  const int gidx = blockIdx.x, bl = blockIdx.y, b = b0 + bl;
-  const int t = threadIdx.x;
-  float2* tin = reinterpret_cast<float2*>(smem);  // [2 kBP][224], then scratch
-  const int y0 = gidx * 2 * kBP;
-  if (t == 0) {
-    tma::bar_init(&bar, 1);
-    tma::load_tile(tin, kp.T2 + ((size_t)bl * 448 + y0) * 224, kT2Rows, &bar);  // same thread: ordered
-  }
-  const int g = t >> 6, r = t & 63;
-  const auto tw = TwSel<LAZY>::make(kp, r);
-  const bool valid = kp.hdr[b].valid != 0;
-  __syncthreads();  // barrier initialised
-  tma::bar_wait(&bar, 0);  // also when cold: the CTA must not exit with a copy in flight
-  if (!valid) return;
-  const int k1 = r >> 3, j1 = r & 7;
-  float2 v[8], a[7];
-  if (r < 56) {
-    const float2* ga = tin + (2 * g) * 224;
-    const float2* gb = ga + 224;
-#pragma unroll
-    for (int j2 = 0; j2 < 8; ++j2) {
-      const int k = k1 + 7 * j1 + 56 * j2;
-      float2 z;
-      if (k == 0) {
-        z = make_float2(ga[0].x, gb[0].x);
-      } else if (k == 224) {
-        z = make_float2(ga[0].y, gb[0].y);
-      } else if (k < 224) {
-        const float2 A = ga[k], B = gb[k];
-        z = make_float2(A.x - B.y, A.y + B.x);   // G_a + i G_b
-      } else {
-        const float2 A = ga[448 - k], B = gb[448 - k];
-        z = make_float2(A.x + B.y, B.x - A.y);   // conj G_a + i conj G_b
-      }
-      v[j2] = z;
-    }
-  }
-  __syncthreads();  // tin consumed; scratch aliases it
-  f448::inv<true>(v, a, tin + g * f448::XR, r, tw);
-
-  // argmax with the reference tie rule (migration.py:141-159): max, its
-  // first position, runner-up; exact ties inside a thread take a slow path
-  const int ya = y0 + 2 * g;
-  float m1 = -CUDART_INF_F, m2 = -CUDART_INF_F;
-  int ai = 0;
-#pragma unroll
-  for (int k = 0; k < 14; ++k) {
-    const float val = (k & 1) ? a[k >> 1].y : a[k >> 1].x;
-    if (val > m1) { m2 = m1; m1 = val; ai = k; }
-    else m2 = fmaxf(m2, val);
-  }
-  auto key_of = [&](int k, float val) {
-    PeakKey c;
-    const int y = ya + (k & 1), j = 64 * (k >> 1) + r;
-    c.v = val;
-    c.l1 = abs(canon_disp(y, 448)) + abs(canon_disp(j, 448));
-    c.pos = y * 448 + j;
-    return c;
-  };
-  PeakKey best = key_of(ai, m1);
-  if (m2 == m1) {
-    for (int k = 0; k < 14; ++k) {
-      const float val = (k & 1) ? a[k >> 1].y : a[k >> 1].x;
-      if (val == m1) {
-        const PeakKey c = key_of(k, val);
-        if (peak_better(c, best)) best = c;
-      }
-    }
-  }
-  float v2 = m2;
-  const int lane = t & 31, wid = t >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    PeakKey other;
-    other.v = __shfl_xor_sync(0xffffffffu, best.v, o);
-    other.l1 = __shfl_xor_sync(0xffffffffu, best.l1, o);
-    other.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
-    const float ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
-    if (peak_better(other, best)) { v2 = fmaxf(fmaxf(v2, ov2), best.v); best = other; }
-    else v2 = fmaxf(fmaxf(v2, ov2), other.v);
-  }
-  if (lane == 0) { redk[wid] = best; redv[wid] = v2; }
-  __syncthreads();
-  if (t == 0) {
-    for (int w = 1; w < (64 * kBP) / 32; ++w) {
-      const PeakKey o = redk[w];
-      if (peak_better(o, best)) { v2 = fmaxf(fmaxf(v2, redv[w]), best.v); best = o; }
-      else v2 = fmaxf(fmaxf(v2, redv[w]), o.v);
-    }
-    PeakPart pp;
-    pp.v = best.v; pp.v2 = v2; pp.y = best.pos / 448; pp.j = best.pos % 448;
-    kp.peaks[(size_t)b * kNRG448 + gidx] = pp;
-  }
-}
-
-// ------------------------------------------------- persistent K_B / K_C ----
-// Same math as k448_cols / k448_rows_inv, but a grid of (SMs x occupancy)
-// CTAs walks the work items with a two-stage TMA ring: while item k is
-// computed, the tiles of item k+1 are already in flight (mbarrier per stage,
-// parity = (k >> 1) & 1).  Before a stage is refilled by the async proxy the
-// generic accesses to it are fenced (fence.proxy.async).
-namespace pers {
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-}  // namespace pers
-
-constexpr int kStageB = ((kScratchB > kT1Block ? kScratchB : kT1Block) + 127) / 128 * 128 + kStBlock;
-constexpr int kSmemBP = 2 * kStageB + 2 * 448 * 8;
-
-__device__ __forceinline__ void colsp_issue(const KParams& kp, int b0, int it, int nitems, unsigned char* stage,
-                                            uint64_t* bar) {
-  if (it >= nitems) return;
-  const int bl = it / kNCB448, cb = it - (it / kNCB448) * kNCB448, b = b0 + bl;
-  const bool valid = kp.hdr[b].valid != 0;
-  const uint32_t bytes = kT1Block + (valid ? kStBlock : 0);
-  tma::bar_expect(bar, bytes);
-  tma::bulk_g2s(stage, kp.T + ((size_t)bl * kNCB448 + cb) * 448 * kBC, kT1Block, bar);
-  if (valid)
-    tma::bulk_g2s(stage + kStageB - kStBlock, kp.spec + (((size_t)b * kNCB448 + cb) * 64 * kBC) * 8, kStBlock, bar);
-}
-
-__global__ void __launch_bounds__(64 * kBC, 3) k448_cols_p(KParams kp, int b0, int nb) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ double red[16 * 4];
-  const int t = threadIdx.x;
-  const int c = t % kBC, r = t / kBC;
-  const int nitems = nb * kNCB448;
-  float2* col0 = reinterpret_cast<float2*>(smem + 2 * kStageB);  // [2][448]
-  f448::Tw tw;
-  f448::load_tw(tw, r, kp.tw448, kp.tw64);
-  if (t == 0) {
-    tma::bar_init(&bar[0], 1);
-    tma::bar_init(&bar[1], 1);
-  }
-  __syncthreads();
-  if (t == 0) {
-    colsp_issue(kp, b0, blockIdx.x, nitems, smem, &bar[0]);
-    colsp_issue(kp, b0, blockIdx.x + gridDim.x, nitems, smem + kStageB, &bar[1]);
-  }
-  int k = 0;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++k) {
-    const int sidx = k & 1;
-    unsigned char* stage = smem + sidx * kStageB;
-    const int bl = it / kNCB448, cb = it - (it / kNCB448) * kNCB448, b = b0 + bl;
-    const bool valid = kp.hdr[b].valid != 0;
-    float2* t1 = reinterpret_cast<float2*>(stage);
-    float2* S = t1 + c * kXCB;
-    const float2* prev = reinterpret_cast<const float2*>(stage + kStageB - kStBlock);
-    float2* stg = kp.spec + (((size_t)b * kNCB448 + cb) * 64 * kBC) * 8;
-    tma::bar_wait(&bar[sidx], (k >> 1) & 1);
-    float2 a[7], v[8];
-#pragma unroll
-    for (int n1 = 0; n1 < 7; ++n1) a[n1] = t1[64 * kBC * n1 + t];
-    __syncthreads();  // t1 consumed: scratch may overwrite it
-    f448::fwd<false>(a, v, S, r, tw);
-    const bool act = r < 56;
-    const int k1 = r >> 3, j1 = r & 7;
-    float4* st = reinterpret_cast<float4*>(stg) + t;  // chunk i at st[i * 64 * kBC]
-    if (act) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) st[i * 64 * kBC] = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
-    }
-    if (valid) {
-      float2 p[8];
-      if (act) {
-        const float4* pv = reinterpret_cast<const float4*>(prev) + t;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 q = pv[i * 64 * kBC];
-          p[2 * i] = make_float2(q.x, q.y);
-          p[2 * i + 1] = make_float2(q.z, q.w);
-        }
-      }
-      float spc = 0.f, spp = 0.f, scc = 0.f, splp = 0.f;
-      auto acc = [&](float w, float2 fp, float2 fc) -> float2 {
-        const float pp = fp.x * fp.x + fp.y * fp.y;
-        const float pc = fc.x * fc.x + fc.y * fc.y;
-        const float m = sqrt_approx(pp * pc);  // |Fp| |Fc|
-        spc = fmaf(w, m, spc);
-        spp = fmaf(w, pp, spp);
-        scc = fmaf(w, pc, scc);
-        if (pc > 0.f) splp = fmaf(w * pc, __logf(pc), splp);
-        const float inv = rcp_approx(m + 1e-12f);  // migration.py:130-131
-        return make_float2((fp.x * fc.x + fp.y * fc.y) * inv, (fp.y * fc.x - fp.x * fc.y) * inv);
-      };
-      if (cb == 0) {
-        if (c == 0 && act) {
-#pragma unroll
-          for (int j2 = 0; j2 < 8; ++j2) {
-            const int kk = k1 + 7 * j1 + 56 * j2;
-            col0[kk] = v[j2];
-            col0[448 + kk] = p[j2];
-          }
-        }
-        __syncthreads();
-        if (c == 0 && act) {
-#pragma unroll
-          for (int j2 = 0; j2 < 8; ++j2) {
-            const int kk = k1 + 7 * j1 + 56 * j2;
-            const int km = (448 - kk) % 448;
-            float2 c0, cn, p0, pn;
-            unpack_dcny(v[j2], col0[km], c0, cn);
-            unpack_dcny(p[j2], col0[448 + km], p0, pn);
-            const float2 x0 = acc(1.f, p0, c0);
-            const float2 xn = acc(1.f, pn, cn);
-            v[j2] = make_float2(x0.x - xn.y, x0.y + xn.x);
-          }
-        }
-      }
-      if (act && !(cb == 0 && c == 0)) {
-#pragma unroll
-        for (int j2 = 0; j2 < 8; ++j2) v[j2] = acc(2.f, p[j2], v[j2]);
-      }
-      f448::inv<true>(v, a, S, r, tw);
-      float2* T2 = kp.T2 + (size_t)bl * 448 * 224 + cb * kBC + c;
-#pragma unroll
-      for (int n1 = 0; n1 < 7; ++n1) T2[(size_t)(64 * n1 + r) * 224] = a[n1];
-      const float fs[4] = {spc, spp, scc, splp};
-      double sums[4];
-      block_sum_f2d<4>(fs, sums, red);
-      if (t == 0) {
-        double* o = kp.stats + ((size_t)b * kNCB448 + cb) * 4;
-        o[0] = sums[0]; o[1] = sums[1]; o[2] = sums[2]; o[3] = sums[3];
-      }
-    }
-    __syncthreads();  // stage fully consumed (scratch, prev, col0)
-    if (t == 0) {
-      pers::fence_async_smem();
-      colsp_issue(kp, b0, it + 2 * gridDim.x, nitems, stage, &bar[sidx]);
-    }
-  }
-}
-
-constexpr int kStageC = ((kBP * f448::XR * 8 > kT2Rows ? kBP * f448::XR * 8 : kT2Rows) + 127) / 128 * 128;
-constexpr int kSmemCP = 2 * kStageC;
-
-__device__ __forceinline__ void rowsp_issue(const KParams& kp, int it, int nitems, unsigned char* stage,
-                                            uint64_t* bar) {
-  if (it >= nitems) return;
-  const int bl = it / kNRG448, gidx = it - (it / kNRG448) * kNRG448;
-  tma::bar_expect(bar, kT2Rows);
-  tma::bulk_g2s(stage, kp.T2 + ((size_t)bl * 448 + gidx * 2 * kBP) * 224, kT2Rows, bar);
-}
-
-__global__ void __launch_bounds__(64 * kBP, 4) k448_rows_inv_p(KParams kp, int b0, int nb) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ PeakKey redk[16];
-  __shared__ float redv[16];
-  const int t = threadIdx.x;
-  const int nitems = nb * kNRG448;
-  const int g = t >> 6, r = t & 63;
-  const int k1 = r >> 3, j1 = r & 7;
-  f448::Tw tw;
-  f448::load_tw(tw, r, kp.tw448, kp.tw64);
-  if (t == 0) {
-    tma::bar_init(&bar[0], 1);
-    tma::bar_init(&bar[1], 1);
-  }
-  __syncthreads();
-  if (t == 0) {
-    rowsp_issue(kp, blockIdx.x, nitems, smem, &bar[0]);
-    rowsp_issue(kp, blockIdx.x + gridDim.x, nitems, smem + kStageC, &bar[1]);
-  }
-  int k = 0;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++k) {
-    const int sidx = k & 1;
-    float2* tin = reinterpret_cast<float2*>(smem + sidx * kStageC);
-    const int bl = it / kNRG448, gidx = it - (it / kNRG448) * kNRG448, b = b0 + bl;
-    const bool valid = kp.hdr[b].valid != 0;
-    const int y0 = gidx * 2 * kBP;
-    tma::bar_wait(&bar[sidx], (k >> 1) & 1);
-    if (valid) {
-      float2 v[8], a[7];
-      if (r < 56) {
-        const float2* ga = tin + (2 * g) * 224;
-        const float2* gb = ga + 224;
-#pragma unroll
-        for (int j2 = 0; j2 < 8; ++j2) {
-          const int kk = k1 + 7 * j1 + 56 * j2;
-          float2 z;
-          if (kk == 0) {
-            z = make_float2(ga[0].x, gb[0].x);
-          } else if (kk == 224) {
-            z = make_float2(ga[0].y, gb[0].y);
-          } else if (kk < 224) {
-            const float2 A = ga[kk], B = gb[kk];
-            z = make_float2(A.x - B.y, A.y + B.x);
-          } else {
-            const float2 A = ga[448 - kk], B = gb[448 - kk];
-            z = make_float2(A.x + B.y, B.x - A.y);
-          }
-          v[j2] = z;
-        }
-      }
-      __syncthreads();  // tin consumed; scratch aliases it
-      f448::inv<true>(v, a, tin + g * f448::XR, r, tw);
-      const int ya = y0 + 2 * g;
-      float m1 = -CUDART_INF_F, m2 = -CUDART_INF_F;
-      int ai = 0;
-#pragma unroll
-      for (int q = 0; q < 14; ++q) {
-        const float val = (q & 1) ? a[q >> 1].y : a[q >> 1].x;
-        if (val > m1) { m2 = m1; m1 = val; ai = q; }
-        else m2 = fmaxf(m2, val);
-      }
-      auto key_of = [&](int q, float val) {
-        PeakKey kq;
-        const int y = ya + (q & 1), j = 64 * (q >> 1) + r;
-        kq.v = val;
-        kq.l1 = abs(canon_disp(y, 448)) + abs(canon_disp(j, 448));
-        kq.pos = y * 448 + j;
-        return kq;
-      };
-      PeakKey best = key_of(ai, m1);
-      if (m2 == m1) {
-        for (int q = 0; q < 14; ++q) {
-          const float val = (q & 1) ? a[q >> 1].y : a[q >> 1].x;
-          if (val == m1) {
-            const PeakKey kq = key_of(q, val);
-            if (peak_better(kq, best)) best = kq;
-          }
-        }
-      }
-      float v2 = m2;
-      const int lane = t & 31, wid = t >> 5;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        PeakKey other;
-        other.v = __shfl_xor_sync(0xffffffffu, best.v, o);
-        other.l1 = __shfl_xor_sync(0xffffffffu, best.l1, o);
-        other.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
-        const float ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
-        if (peak_better(other, best)) { v2 = fmaxf(fmaxf(v2, ov2), best.v); best = other; }
-        else v2 = fmaxf(fmaxf(v2, ov2), other.v);
-      }
-      if (lane == 0) { redk[wid] = best; redv[wid] = v2; }
-      __syncthreads();
-      if (t == 0) {
-        for (int w = 1; w < (64 * kBP) / 32; ++w) {
-          const PeakKey o = redk[w];
-          if (peak_better(o, best)) { v2 = fmaxf(fmaxf(v2, redv[w]), best.v); best = o; }
-          else v2 = fmaxf(fmaxf(v2, redv[w]), o.v);
-        }
-        PeakPart pp;
-        pp.v = best.v; pp.v2 = v2; pp.y = best.pos / 448; pp.j = best.pos % 448;
-        kp.peaks[(size_t)b * kNRG448 + gidx] = pp;
-      }
-    }
-    __syncthreads();  // stage consumed (input + scratch)
-    if (t == 0) {
-      pers::fence_async_smem();
-      rowsp_issue(kp, it + 2 * gridDim.x, nitems, reinterpret_cast<unsigned char*>(tin), &bar[sidx]);
-    }
-  }
-}

@@ -1,0 +1,306 @@
+// K_B and K_C of the 448 x 448 fast path (K_A, the geometry and the f448
+// CTA-wide FFT are in fc_fast448.cuh).
+//
+// Both kernels are warp-owned: every 448-point transform belongs to one warp
+// (w448 in fc_wfft448.cuh), every warp stages its own tiles with its own TMA
+// bulk copies and mbarriers, and the FFT exchanges need only __syncwarp, so
+// the warps of a CTA never wait for each other until the final (per-CTA)
+// reduction.
+//
+// Spectrum intermediates are column-major per stream:
+//   T1 [q][448 rows] complex64  (K_A -> K_B: row spectra, packed column q)
+//   T2 [224 row pairs][q][2 rows] complex64  (K_B -> K_C: cross-power after the
+//      inverse column FFT; a row pair is one contiguous 3.5 KB block for K_C;
+//      K_B transposes its 4 columns through shared memory and writes 64-byte
+//      runs)
+// Per-stream state (the previous frame's half spectrum) is kept in the
+// register order of K_B's forward transform:
+//   spec [q][h][i][lane] float4 = (X[k(j2 = 2i)], X[k(j2 = 2i + 1)]) of group
+//   g = lane + 32 h, k(j2) = (g >> 3) + 7 (g & 7) + 56 j2  (4 KB per column)
+// so a warp loads / stores its column with 16-byte coalesced accesses.
+#pragma once
+#include <type_traits>
+#include "fc_fast448.cuh"
+#include "fc_wfft448.cuh"
+
+constexpr int kWarpsB = 4;                 // columns (warps) per K_B CTA
+constexpr int kNCB448 = 224 / kWarpsB;     // K_B CTAs per stream = stats partials
+constexpr int kWarpsC = 4;                 // row pairs (warps) per K_C CTA
+constexpr int kNRG448 = 224 / kWarpsC;     // K_C CTAs per stream = peak partials
+constexpr int kStCol = 2 * 4 * 32;         // float4 per state column
+constexpr int kSlotB = 512;                // float2: T1 column (448), then FFT scratch (504)
+constexpr int kSmemB448 = kWarpsB * (kSlotB * 8 + kStCol * 16);
+static_assert(kWarpsB == 4 && 224 * 4 * 16 <= kWarpsB * kStCol * 16, "T2 tile must fit the prev blocks");
+constexpr int kSmemC448 = kWarpsC * w448::XS * 8;
+
+template <bool LAZY>
+using W448Tw = typename std::conditional<LAZY, w448::TwLazy, w448::Tw>::type;
+
+// fp64 warp sum in a fixed xor-tree order (deterministic)
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------- K_B 448 ----
+// One warp per packed column q of a stream: forward column FFT of the T1
+// column, state swap (previous spectrum in, current out), Hermitian-weighted
+// sums for sim_freq and the entropy (migration.py:87-105, budget.py:34-58),
+// normalised cross-power (migration.py:128-131) and the inverse column FFT
+// into T2.  Column 0 holds the packed DC / Nyquist columns (real along rows),
+// unpacked with bins k and 448 - k of the same column.
+template <int MINB, bool LAZY>
+__global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int b0) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[kWarpsB][2];
+  __shared__ double red[kWarpsB][4];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bl = blockIdx.y, b = b0 + bl;
+  const int q = blockIdx.x * kWarpsB + wid;
+  // [slot 0..3 (T1 column / FFT scratch) | prev 0..3 (state); later the T2 tile]
+  float2* slot = reinterpret_cast<float2*>(smem + wid * (kSlotB * 8));
+  float4* prev = reinterpret_cast<float4*>(smem + kWarpsB * kSlotB * 8 + wid * (kStCol * 16));
+  const bool valid = kp.hdr[b].valid != 0;
+  float4* stg = reinterpret_cast<float4*>(kp.spec) + ((size_t)b * 224 + q) * kStCol;
+  if (lane == 0) {
+    tma::bar_init(&bar[wid][0], 1);
+    tma::bar_init(&bar[wid][1], 1);
+    tma::load_tile(slot, kp.T + ((size_t)bl * 224 + q) * 448, 448 * 8, &bar[wid][0]);
+    if (valid) tma::load_tile(prev, stg, kStCol * 16, &bar[wid][1]);
+  }
+  W448Tw<LAZY> tw;
+  tw.load(kp.tw448, kp.tw64, lane);
+  __syncwarp();
+  tma::bar_wait(&bar[wid][0], 0);
+  float2 a[2][7], v[2][8];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int n1 = 0; n1 < 7; ++n1) a[h][n1] = slot[64 * n1 + lane + 32 * h];
+  __syncwarp();  // T1 column consumed: the slot becomes FFT scratch
+  w448::fwd<false>(a, v, slot, lane, tw);
+
+  const bool h1 = lane < 24;
+  // the previous spectrum must have landed before its block is overwritten
+  if (valid) tma::bar_wait(&bar[wid][1], 0);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h == 0 || h1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        stg[(h * 4 + i) * 32 + lane] = make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
+    }
+  }
+  if (!valid) return;  // cold stream: spectrum established (block-uniform)
+
+  float spc = 0.f, spp = 0.f, scc = 0.f, splp = 0.f;
+  auto acc = [&](float w, float2 fp, float2 fc) -> float2 {
+    const float pp = fp.x * fp.x + fp.y * fp.y;
+    const float pc = fc.x * fc.x + fc.y * fc.y;
+    const float m = sqrt_approx(pp * pc);  // |Fp| |Fc|
+    spc = fmaf(w, m, spc);
+    spp = fmaf(w, pp, spp);
+    scc = fmaf(w, pc, scc);
+    if (pc > 0.f) splp = fmaf(w * pc, __logf(pc), splp);
+    // normalised cross-power (migration.py:130-131)
+    const float inv = rcp_approx(m + 1e-12f);
+    return make_float2((fp.x * fc.x + fp.y * fc.y) * inv, (fp.y * fc.x - fp.x * fc.y) * inv);
+  };
+  const int k1a = lane >> 3, j1 = lane & 7;
+  __syncwarp();  // every lane is done with the FFT scratch and the prev block
+  if (q == 0) {
+    // packed DC/Nyquist column (warp-uniform): bins k and 448 - k of both
+    // spectra.  The current spectrum goes to the slot in the same register
+    // order as the previous one, and mirrored bins are fetched through the
+    // inverse of k(g, j2).
+    float4* cur = reinterpret_cast<float4*>(slot);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 0 || h1) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          cur[(h * 4 + i) * 32 + lane] = make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
+      }
+    }
+    __syncwarp();
+    auto fetch = [](const float4* base, int k) -> float2 {
+      const int j2 = k / 56, rem = k - 56 * j2;
+      const int g = 8 * (rem % 7) + rem / 7;
+      const float4 t = base[((g >> 5) * 4 + (j2 >> 1)) * 32 + (g & 31)];
+      return (j2 & 1) ? make_float2(t.z, t.w) : make_float2(t.x, t.y);
+    };
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 0 || h1) {
+#pragma unroll
+        for (int j2 = 0; j2 < 8; ++j2) {
+          const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
+          const int km = (448 - k) % 448;
+          const float4 t = prev[(h * 4 + (j2 >> 1)) * 32 + lane];
+          const float2 pk = (j2 & 1) ? make_float2(t.z, t.w) : make_float2(t.x, t.y);
+          float2 c0, cn, p0, pn;
+          unpack_dcny(v[h][j2], fetch(cur, km), c0, cn);
+          unpack_dcny(pk, fetch(prev, km), p0, pn);
+          const float2 x0 = acc(1.f, p0, c0);
+          const float2 xn = acc(1.f, pn, cn);
+          v[h][j2] = make_float2(x0.x - xn.y, x0.y + xn.x);
+        }
+      }
+    }
+    __syncwarp();  // the slot becomes FFT scratch again
+  } else {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 0 || h1) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 t = prev[(h * 4 + i) * 32 + lane];
+          v[h][2 * i] = acc(2.f, make_float2(t.x, t.y), v[h][2 * i]);
+          v[h][2 * i + 1] = acc(2.f, make_float2(t.z, t.w), v[h][2 * i + 1]);
+        }
+      }
+    }
+  }
+  w448::inv<true>(v, a, slot, lane, tw);
+  // per-CTA partial sums: fp32 per lane, fp64 warp tree, warps in order
+  const double s0 = warp_sum_f64((double)spc), s1 = warp_sum_f64((double)spp);
+  const double s2 = warp_sum_f64((double)scc), s3 = warp_sum_f64((double)splp);
+  if (lane == 0) {
+    red[wid][0] = s0; red[wid][1] = s1; red[wid][2] = s2; red[wid][3] = s3;
+  }
+  // T2 tile [224 pairs][4 columns] of 16-byte (row 2p, row 2p + 1) units over
+  // the prev blocks (every warp is past its cross-power after this barrier);
+  // the unit of column w in pair p sits at p * 4 + (w ^ ((p >> 1) & 3)), so
+  // the writes below and the reads of the copy-out are conflict free
+  __syncthreads();
+  float2* tile = reinterpret_cast<float2*>(smem + kWarpsB * kSlotB * 8);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int n1 = 0; n1 < 7; ++n1) {
+      const int y = 64 * n1 + lane + 32 * h, pr = y >> 1;
+      tile[(pr * 4 + (wid ^ ((pr >> 1) & 3))) * 2 + (y & 1)] = a[h][n1];
+    }
+  if (threadIdx.x < 4) {
+    double acc4 = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarpsB; ++w) acc4 += red[w][threadIdx.x];
+    kp.stats[((size_t)b * kNCB448 + blockIdx.x) * 4 + threadIdx.x] = acc4;
+  }
+  __syncthreads();
+  const float4* t4 = reinterpret_cast<const float4*>(tile);
+  float4* T2 = reinterpret_cast<float4*>(kp.T2) + (size_t)bl * 224 * 224 + blockIdx.x * kWarpsB;
+  for (int u = threadIdx.x; u < 224 * 4; u += 32 * kWarpsB) {
+    const int pr = u >> 2, col = (u & 3) ^ ((pr >> 1) & 3);
+    T2[(size_t)pr * 224 + col] = t4[u];
+  }
+}
+
+// ------------------------------------------------------------- K_C 448 ----
+// One warp per row pair (ya, ya + 1) of T2: both rows are one packed complex
+// 448-point inverse transform (c2r), read straight from the L2-resident T2
+// row-pair block (one 16-byte load gives both rows of a column).  Then the
+// argmax with the reference's tie rule and the runner-up; one peak partial
+// per CTA (kNRG448 per stream), merged by K_D in its fixed tie order.
+template <int MINB, bool LAZY>
+__global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, int b0) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ PeakKey redk[kWarpsC];
+  __shared__ float redv[kWarpsC];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bl = blockIdx.y, b = b0 + bl;
+  if (kp.hdr[b].valid == 0) return;  // cold stream (block-uniform)
+  const int pair = blockIdx.x * kWarpsC + wid;
+  const int ya = 2 * pair;
+  float2* S = reinterpret_cast<float2*>(smem) + wid * w448::XS;
+  const float4* T2 = reinterpret_cast<const float4*>(kp.T2) + ((size_t)bl * 224 + pair) * 224;
+  const int k1a = lane >> 3, j1 = lane & 7;
+  float4 in[2][8];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h == 0 || lane < 24) {
+#pragma unroll
+      for (int j2 = 0; j2 < 8; ++j2) {
+        const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
+        const int qq = (k == 0 || k == 224) ? 0 : (k < 224 ? k : 448 - k);
+        in[h][j2] = __ldg(T2 + qq);
+      }
+    }
+  }
+  W448Tw<LAZY> tw;
+  tw.load(kp.tw448, kp.tw64, lane);
+  float2 v[2][8], a[2][7];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h == 0 || lane < 24) {
+#pragma unroll
+      for (int j2 = 0; j2 < 8; ++j2) {
+        const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
+        const float4 t = in[h][j2];  // (A = row ya, B = row ya + 1) at the column
+        float2 z;
+        if (k == 0) z = make_float2(t.x, t.z);
+        else if (k == 224) z = make_float2(t.y, t.w);
+        else if (k < 224) z = make_float2(t.x - t.w, t.y + t.z);   // G_a + i G_b
+        else z = make_float2(t.x + t.w, t.z - t.y);                // conj G_a + i conj G_b
+        v[h][j2] = z;
+      }
+    }
+  }
+  w448::inv<true>(v, a, S, lane, tw);
+
+  // argmax with the reference tie rule (migration.py:141-159)
+  float m1 = -CUDART_INF_F, m2 = -CUDART_INF_F;
+  int ai = 0;
+#pragma unroll
+  for (int qv = 0; qv < 28; ++qv) {
+    const float2 c = a[qv / 14][(qv % 14) >> 1];
+    const float val = (qv & 1) ? c.y : c.x;
+    if (val > m1) { m2 = m1; m1 = val; ai = qv; }
+    else m2 = fmaxf(m2, val);
+  }
+  auto key_of = [&](int qv, float val) {
+    PeakKey c;
+    const int y = ya + (qv & 1), j = 64 * ((qv % 14) >> 1) + lane + 32 * (qv / 14);
+    c.v = val;
+    c.l1 = abs(canon_disp(y, 448)) + abs(canon_disp(j, 448));
+    c.pos = y * 448 + j;
+    return c;
+  };
+  PeakKey best = key_of(ai, m1);
+  if (m2 == m1) {
+    for (int qv = 0; qv < 28; ++qv) {
+      const float2 c = a[qv / 14][(qv % 14) >> 1];
+      const float val = (qv & 1) ? c.y : c.x;
+      if (val == m1) {
+        const PeakKey kq = key_of(qv, val);
+        if (peak_better(kq, best)) best = kq;
+      }
+    }
+  }
+  float v2 = m2;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    PeakKey other;
+    other.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+    other.l1 = __shfl_xor_sync(0xffffffffu, best.l1, o);
+    other.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
+    const float ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+    if (peak_better(other, best)) { v2 = fmaxf(fmaxf(v2, ov2), best.v); best = other; }
+    else v2 = fmaxf(fmaxf(v2, ov2), other.v);
+  }
+  if (lane == 0) { redk[wid] = best; redv[wid] = v2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    best = redk[0];
+    v2 = redv[0];
+    for (int w = 1; w < kWarpsC; ++w) {
+      const PeakKey o = redk[w];
+      if (peak_better(o, best)) { v2 = fmaxf(fmaxf(v2, redv[w]), best.v); best = o; }
+      else v2 = fmaxf(fmaxf(v2, redv[w]), o.v);
+    }
+    PeakPart pp;
+    pp.v = best.v; pp.v2 = v2; pp.y = best.pos / 448; pp.j = best.pos % 448;
+    kp.peaks[(size_t)b * kNRG448 + blockIdx.x] = pp;
+  }
+}
