@@ -193,7 +193,7 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
       KParams kl = kp;
       kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride);
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
-      fa<<<dim3(32, nb), 448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1);
+      fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1);
       if (rec) rec->mark(st, 0);
       auto fb = (void (*)(KParams, int))pl->fnB;
       fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0);
@@ -460,7 +460,7 @@ int fc_patch_energy(const fc_plan* pl, const void* frames, void* ws, double* ene
   const cudaStream_t st = as_stream(stream);
   if (pl->fast) {
     auto fn = (void (*)(KParams, Dct14, const void*, int, int))sel_fast_rows_fwd(pl->g.format);
-    fn<<<dim3(32, pl->g.batch), 448, pl->smemA, st>>>(kp, pl->dct14, frames, 0, 0);
+    fn<<<dim3(32, pl->g.batch), kThreadsA448, pl->smemA, st>>>(kp, pl->dct14, frames, 0, 0);
   } else {
     auto fn = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
     fn<<<dim3(kp.rows, pl->g.batch), FC_THREADS, pl->smemA, st>>>(kp, frames, 0);

@@ -17,6 +17,7 @@
 #pragma once
 #include "fc_fft.cuh"
 #include "fc_tma.cuh"
+#include "fc_wfft448.cuh"
 
 namespace f448 {
 
@@ -158,103 +159,128 @@ struct Dct14 {
 };
 
 // ------------------------------------------------------------- K_A 448 ----
-// One CTA per (stripe of 14 rows, stream); 448 threads.
-// phase 0: TMA bulk copy of the stripe (two 7-row halves, two mbarriers);
-// phase 1: thread = column: pixels -> fp64 luma (14 rows), flags, DCT
-//          partials T[u][col] = sum_x C[u][x] X[x][col], s2[col] = sum_x X^2
-//          (fp64), fp32 gray pairs for the FFT;
+// One CTA per (stripe of 14 rows, stream); 7 warps, warp g owns row pair
+// (2g, 2g + 1) for the FFT, thread t owns columns (2t, 2t + 1) for the DCT.
+// phase 0: TMA bulk copies of the stripe, one per row pair (7 mbarriers), so
+//          phase 1 starts on the first pair while the rest is in flight;
+// phase 1: thread = column pair: pixels -> fp64 luma, flags, DCT partials
+//          T[u][col] = sum_x C[u][x] X[x][col], s2[col] = sum_x X^2 (fp64),
+//          fp32 gray kept for the FFT;
 // phase 2: E = sum s2 - sum_{u,v<3} (sum_y T[u][y] C[v][y])^2 per patch;
-// phase 3: 7 packed-pair forward FFTs (row pairs as complex);
+// phase 3: warp g: packed-pair forward FFT of rows (2g, 2g + 1) (w448);
 // phase 4: split pairs, write packed half-spectrum columns to T1, which is
 //          column-major ([stream][q][448 rows] complex64): K_B stages one
 //          contiguous 3.5 KB column per warp.
 constexpr int kPxBytes448 = 14 * 448 * 12;  // largest stripe (fp32 RGB)
-static_assert(448 * 9 * 8 <= 7 * 448 * 8 + (4 * 480 + 288) * 8, "zout must not reach the FFT scratch");
+constexpr int kThreadsA448 = 224;
+// shared memory after phase 1 (aliasing the consumed stripe):
+// [zin 7x448 | part 4x(32x15) + ysq 9x32 (fp64)] then zout [448][9] over
+// both, and the per-warp FFT scratch 7 x 504 after them
+constexpr int kZinBytes = 7 * 448 * 8;
+constexpr int kPartBytes = (4 * 480 + 288) * 8;
+static_assert(448 * 9 * 8 <= kZinBytes + kPartBytes, "zout must not reach the FFT scratch");
+static_assert(kZinBytes + kPartBytes + 7 * 504 * 8 <= kPxBytes448, "K_A shared memory");
 
+// Gray values of two horizontally adjacent pixels i, i + 1 (i even).
 template <int FMT>
-__device__ __forceinline__ double smem_luma(const unsigned char* px, int i) {
+__device__ __forceinline__ void smem_luma2(const unsigned char* px, int i, double& v0, double& v1) {
   if constexpr (FMT == FC_FMT_RGB_F32) {
-    const float* f = reinterpret_cast<const float*>(px) + 3 * i;
-    return luma_f64(f[0], f[1], f[2]);
+    const float2* f = reinterpret_cast<const float2*>(px + 12 * (size_t)i);
+    const float2 a = f[0], b = f[1], c = f[2];  // R0 G0 | B0 R1 | G1 B1
+    v0 = luma_f64(a.x, a.y, b.x);
+    v1 = luma_f64(b.y, c.x, c.y);
   } else if constexpr (FMT == FC_FMT_GRAY_F32) {
-    return (double)reinterpret_cast<const float*>(px)[i];
+    const float2 f = *reinterpret_cast<const float2*>(px + 4 * (size_t)i);
+    v0 = (double)f.x;
+    v1 = (double)f.y;
   } else if constexpr (FMT == FC_FMT_GRAY_U8) {
-    return gray_u8(px[i]);
+    v0 = gray_u8(px[i]);
+    v1 = gray_u8(px[i + 1]);
   } else if constexpr (FMT == FC_FMT_RGB_U8) {
-    return luma_u8(px[3 * i], px[3 * i + 1], px[3 * i + 2]);
+    const unsigned char* q = px + 3 * (size_t)i;
+    v0 = luma_u8(q[0], q[1], q[2]);
+    v1 = luma_u8(q[3], q[4], q[5]);
   } else {
-    return reinterpret_cast<const double*>(px)[i];
+    const double2 f = *reinterpret_cast<const double2*>(px + 8 * (size_t)i);
+    v0 = f.x;
+    v1 = f.y;
   }
 }
 
 template <int FMT>
-__global__ void __launch_bounds__(448, 3) k448_rows_fwd(KParams kp, Dct14 dc, const void* __restrict__ frames,
-                                                       int b0, int do_fft) {
+__global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct14 dc, const void* __restrict__ frames,
+                                                                int b0, int do_fft) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[7];
   constexpr int bpp = FMT == FC_FMT_RGB_F32 ? 12 : FMT == FC_FMT_GRAY_F32 ? 4 : FMT == FC_FMT_GRAY_U8 ? 1
                     : FMT == FC_FMT_RGB_U8 ? 3 : 8;
+  constexpr uint32_t pair_bytes = 2 * 448 * bpp;
   const int s = blockIdx.x, bl = blockIdx.y, b = b0 + bl;
-  const int t = threadIdx.x;
-  // one 73.5 KB region: the staged stripe, then (after every pixel is read)
-  // [zin 7x448 complex | DCT partials + corner squares | FFT scratch 7x504]
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
   unsigned char* px = smem;
-  float2* zin = reinterpret_cast<float2*>(smem);                      // [7][448]
-  double* part = reinterpret_cast<double*>(smem + 7 * 448 * 8);       // [4][32 x 15]
-  double* ysq = part + 4 * 480;                                       // [9][32]
-  float2* S = reinterpret_cast<float2*>(smem + 7 * 448 * 8 + (4 * 480 + 288) * 8);  // [7][504]
+  float2* zin = reinterpret_cast<float2*>(smem);                     // [7][448]
+  double* part = reinterpret_cast<double*>(smem + kZinBytes);        // [4][32 x 15]
+  double* ysq = part + 4 * 480;                                      // [9][32]
+  float2* S = reinterpret_cast<float2*>(smem + kZinBytes + kPartBytes) + wid * w448::XS;
 
-  // ---- phase 0: stage the stripe with the TMA engine
+  // ---- phase 0: stage the stripe with the TMA engine, one copy per row pair
   const size_t row0 = ((size_t)b * 448 + (size_t)s * 14) * 448;
   if (t == 0) {
-    tma::bar_init(&bar[0], 1);
-    tma::bar_init(&bar[1], 1);
-  }
-  __syncthreads();
-  if (t == 0) {
+#pragma unroll
+    for (int g = 0; g < 7; ++g) tma::bar_init(&bar[g], 1);
     const char* src = reinterpret_cast<const char*>(frames) + row0 * bpp;
-    constexpr uint32_t half_bytes = 7 * 448 * bpp;
-    tma::load_tile(px, src, half_bytes, &bar[0]);
-    tma::load_tile(px + half_bytes, src + half_bytes, half_bytes, &bar[1]);
+#pragma unroll
+    for (int g = 0; g < 7; ++g) tma::load_tile(px + g * pair_bytes, src + g * pair_bytes, pair_bytes, &bar[g]);
   }
+  __syncthreads();  // barriers initialised
 
-  // ---- phase 1
+  // ---- phase 1: thread = columns (2t, 2t + 1)
   bool vary = false;
   unsigned emax = 0u;
   double ref = 0.0;
-  double s2 = 0.0, tu0 = 0.0, tu1 = 0.0, tu2 = 0.0;
-  float g32[14];
+  double s2[2] = {0.0, 0.0}, tu0[2] = {0.0, 0.0}, tu1[2] = {0.0, 0.0}, tu2[2] = {0.0, 0.0};
+  float g32[14][2];
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    tma::bar_wait(&bar[half], 0);
-    if (half == 0) ref = smem_luma<FMT>(px, 0);
+  for (int g = 0; g < 7; ++g) {
+    tma::bar_wait(&bar[g], 0);
+    if (g == 0) {
+      double r1;
+      smem_luma2<FMT>(px, 0, ref, r1);
+    }
 #pragma unroll
-    for (int x = 0; x < 7; ++x) {
-      const int xx = half * 7 + x;
-      const double v = smem_luma<FMT>(px, xx * 448 + t);
-      g32[xx] = (float)v;
-      vary |= (v != ref);
-      emax = max(emax, (unsigned)__double2hiint(v) & 0x7ff00000u);
-      s2 = fma(v, v, s2);
-      tu0 = fma(dc.c[0][xx], v, tu0);
-      tu1 = fma(dc.c[1][xx], v, tu1);
-      tu2 = fma(dc.c[2][xx], v, tu2);
+    for (int x2 = 0; x2 < 2; ++x2) {
+      const int xx = 2 * g + x2;
+      double v[2];
+      smem_luma2<FMT>(px, xx * 448 + 2 * t, v[0], v[1]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        g32[xx][c] = (float)v[c];
+        vary |= (v[c] != ref);
+        emax = max(emax, (unsigned)__double2hiint(v[c]) & 0x7ff00000u);
+        s2[c] = fma(v[c], v[c], s2[c]);
+        tu0[c] = fma(dc.c[0][xx], v[c], tu0[c]);
+        tu1[c] = fma(dc.c[1][xx], v[c], tu1[c]);
+        tu2[c] = fma(dc.c[2][xx], v[c], tu2[c]);
+      }
     }
   }
   const int anyvary = __syncthreads_or(vary);  // also: every pixel has been read
   const int anybad = __syncthreads_or(emax == 0x7ff00000u);
   // fp32 gray as packed row pairs (2g, 2g+1), over the consumed stripe
 #pragma unroll
-  for (int g = 0; g < 7; ++g) zin[g * 448 + t] = make_float2(g32[2 * g], g32[2 * g + 1]);
+  for (int g = 0; g < 7; ++g)
+    *reinterpret_cast<float4*>(zin + g * 448 + 2 * t) =
+        make_float4(g32[2 * g][0], g32[2 * g + 1][0], g32[2 * g][1], g32[2 * g + 1][1]);
   // per-patch stride 15 (one pad double): phase-2 reads of 32 patches hit
   // 16 distinct bank pairs per half-warp
-  {
-    const int pp = t / 14, y = t - (t / 14) * 14;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int col = 2 * t + c, pp = col / 14, y = col - (col / 14) * 14;
     double* pc = part + pp * 15 + y;
-    pc[0 * 480] = tu0;
-    pc[1 * 480] = tu1;
-    pc[2 * 480] = tu2;
-    pc[3 * 480] = s2;
+    pc[0 * 480] = tu0[c];
+    pc[1 * 480] = tu1[c];
+    pc[2 * 480] = tu2[c];
+    pc[3 * 480] = s2[c];
   }
   if (t == 0) {
     StripeStat st;
@@ -263,14 +289,14 @@ __global__ void __launch_bounds__(448, 3) k448_rows_fwd(KParams kp, Dct14 dc, co
     kp.stripes[(size_t)b * 32 + s] = st;
   }
   __syncthreads();
-  // ---- phase 2: low-frequency corner per patch (fp64); warp = (u, v), lane = patch
-  if (t < 288) {
-    const int uv = t >> 5, pp = t & 31, u = uv / 3, v = uv - (uv / 3) * 3;
+  // ---- phase 2: low-frequency corner per patch (fp64); (u, v) x patch
+  for (int i = t; i < 288; i += kThreadsA448) {
+    const int uv = i >> 5, pp = i & 31, u = uv / 3, v = uv - (uv / 3) * 3;
     const double* tp = part + u * 480 + pp * 15;
     double y = 0.0;
 #pragma unroll
     for (int q = 0; q < 14; ++q) y = fma(tp[q], dc.c[v][q], y);
-    ysq[t] = y * y;
+    ysq[i] = y * y;
   }
   __syncthreads();
   if (t < 32) {
@@ -285,29 +311,35 @@ __global__ void __launch_bounds__(448, 3) k448_rows_fwd(KParams kp, Dct14 dc, co
     kp.energy[(size_t)b * 1024 + s * 32 + t] = e > 0.0 ? e : 0.0;
   }
   if (!do_fft) return;
-  __syncthreads();  // part/ysq (aliasing S) consumed
 
-  // ---- phase 3: packed-pair forward FFTs, g = pair, r = role
-  const int g = t >> 6, r = t & 63;
-  float2 a[7], bv[8];
+  // ---- phase 3: warp g = row pair g: packed-pair forward FFT
+  const int g = wid;
+  float2 a[2][7], bv[2][8];
 #pragma unroll
-  for (int n1 = 0; n1 < 7; ++n1) a[n1] = zin[g * 448 + 64 * n1 + r];
-  const f448::TwLazy tw{kp.tw448, kp.tw64, r};
-  f448::fwd<false>(a, bv, S + g * f448::XR, r, tw);
-  // zout[k][9]: bin k of pair g at k * 9 + g (zin and part are consumed; S
-  // may still be read by other transforms, zout does not overlap it)
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int n1 = 0; n1 < 7; ++n1) a[h][n1] = zin[g * 448 + 64 * n1 + lane + 32 * h];
+  w448::TwLazy tw;
+  tw.load(kp.tw448, kp.tw64, lane);
+  w448::fwd<false>(a, bv, S, lane, tw);  // private scratch
+  // zout[k][9]: bin k of pair g at k * 9 + g, over zin and part (every warp
+  // has loaded its zin row and phase 2 is done after this barrier)
+  __syncthreads();
   float2* zout = zin;
-  if (r < 56) {
-    const int k1 = r >> 3, j1 = r & 7;
 #pragma unroll
-    for (int j2 = 0; j2 < 8; ++j2) zout[(k1 + 7 * j1 + 56 * j2) * 9 + g] = bv[j2];
+  for (int h = 0; h < 2; ++h) {
+    if (h == 0 || lane < 24) {
+      const int k1 = (lane >> 3) + 4 * h, j1 = lane & 7;
+#pragma unroll
+      for (int j2 = 0; j2 < 8; ++j2) zout[(k1 + 7 * j1 + 56 * j2) * 9 + g] = bv[h][j2];
+    }
   }
   __syncthreads();
 
   // ---- phase 4: split the two real rows' spectra; consecutive threads take
   // consecutive row pairs of one column, so each column's 14 stripe rows
   // (112 contiguous bytes of T1) are written by neighbouring lanes
-  for (int idx = t; idx < 7 * 224; idx += 448) {
+  for (int idx = t; idx < 7 * 224; idx += kThreadsA448) {
     const int q = idx / 7, gg = idx - (idx / 7) * 7;
     float2 xa, xb;
     if (q == 0) {
@@ -323,4 +355,3 @@ __global__ void __launch_bounds__(448, 3) k448_rows_fwd(KParams kp, Dct14 dc, co
     *reinterpret_cast<float4*>(kp.T + ((size_t)bl * 224 + q) * 448 + ra) = make_float4(xa.x, xa.y, xb.x, xb.y);
   }
 }
-
