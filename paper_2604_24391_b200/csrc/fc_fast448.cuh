@@ -338,20 +338,22 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
 
   // ---- phase 4: split the two real rows' spectra; consecutive threads take
   // consecutive row pairs of one column, so each column's 14 stripe rows
-  // (112 contiguous bytes of T1) are written by neighbouring lanes
-  for (int idx = t; idx < 7 * 224; idx += kThreadsA448) {
-    const int q = idx / 7, gg = idx - (idx / 7) * 7;
-    float2 xa, xb;
-    if (q == 0) {
+  // (112 contiguous bytes of T1) are written by neighbouring lanes.  Thread t
+  // keeps row pair gg = t % 7 and walks columns t / 7 + 32 i (224 = 7 * 32).
+  {
+    const int gg = t % 7, q0 = t / 7;
+    float4* dst = reinterpret_cast<float4*>(kp.T + (size_t)bl * 224 * 448 + s * 14 + 2 * gg);
+    if (q0 == 0) {
       const float2 z0 = zout[gg], zn = zout[224 * 9 + gg];
-      xa = make_float2(z0.x, zn.x);
-      xb = make_float2(z0.y, zn.y);
-    } else {
-      const float2 za = zout[q * 9 + gg], zm = zout[(448 - q) * 9 + gg];
-      xa = make_float2(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y));
-      xb = make_float2(0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
+      dst[0] = make_float4(z0.x, zn.x, z0.y, zn.y);
     }
-    const int ra = s * 14 + 2 * gg;
-    *reinterpret_cast<float4*>(kp.T + ((size_t)bl * 224 + q) * 448 + ra) = make_float4(xa.x, xa.y, xb.x, xb.y);
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      const int q = q0 + 32 * i;
+      if (q == 0) continue;
+      const float2 za = zout[q * 9 + gg], zm = zout[(448 - q) * 9 + gg];
+      dst[(size_t)q * 224] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y),
+                                         0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
+    }
   }
 }
