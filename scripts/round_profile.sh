@@ -18,6 +18,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"
 echo launches_rc=$?
 CMD="python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline"
 timeout 600 $CMD > /dev/null 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"k448_rows_fwd|k448_cols|k448_rows_inv|k_select|k_splice_ip|k_splice_plan" -s 12 -c 12 \
+    -k regex:"k448_rows_fwd|k448_cols|k448_rows_inv|k_select|k_splice_ip|k_splice_plan" -s 12 -c 6 \
     -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 echo full_rc=$?
