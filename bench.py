@@ -437,6 +437,18 @@ def run_ours(a):
     e2e_val = S * ke * world / (float(ems.item()) / 1e3)
     h2d = S * H * H * 3 * 4
     d2h = S * 136 + S * N * 4
+    # the link the e2e number is bound by: plain pinned H2D copy of one step's frames
+    for _ in range(2):
+        stages[0].copy_(host[0], non_blocking=True)
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for i in range(3):
+        stages[i & 1].copy_(host[i % HR], non_blocking=True)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    pcie_gbs = 3 * h2d / (p0.elapsed_time(p1) / 1e3) / 1e9
+    e2e_h2d_gbs = h2d * e2e_val / S / world / 1e9
 
     # ---- single-stream step latency (select + splice), CUDA-graph replay:
     # config 1 (224x224, fixed 50 % budget) and one config-2 stream (448x448)
@@ -504,6 +516,7 @@ def run_ours(a):
             "roofline": roofline, "roofline_step": roofline_step, "kernels": kernels,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "h2d_gbs": e2e_h2d_gbs, "pcie_copy_gbs": pcie_gbs, "link_frac": e2e_h2d_gbs / pcie_gbs,
                     "steps": ke, "path": "pinned host frames -> (copy stream, double-buffered) fc_select -> "
                                          "fc_splice_inplace -> results + splice map to pinned host"},
             "gpu_launches": gpu_launches,
