@@ -94,18 +94,23 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
   }
   if (!valid) return;  // cold stream: spectrum established (block-uniform)
 
+  // Per-lane sums of one column; the Hermitian weight (2, or 1 for the
+  // packed DC / Nyquist column, warp-uniform) and ln 2 are applied once at the
+  // end.  Two MUFU ops per bin: rsqrt(|Fp|^2 |Fc|^2) gives both |Fp||Fc| and
+  // the cross-power normaliser 1 / (|Fp||Fc| + 1e-12) (the 1e-12 only matters
+  // below |Fp||Fc| ~ 1e-8, where the numerator is as small), lg2 the entropy.
   float spc = 0.f, spp = 0.f, scc = 0.f, splp = 0.f;
-  auto acc = [&](float w, float2 fp, float2 fc) -> float2 {
+  auto acc = [&](float2 fp, float2 fc) -> float2 {
     const float pp = fp.x * fp.x + fp.y * fp.y;
     const float pc = fc.x * fc.x + fc.y * fc.y;
-    const float m = sqrt_approx(pp * pc);  // |Fp| |Fc|
-    spc = fmaf(w, m, spc);
-    spp = fmaf(w, pp, spp);
-    scc = fmaf(w, pc, scc);
-    if (pc > 0.f) splp = fmaf(w * pc, __logf(pc), splp);
+    const float x = pp * pc;
+    const float r = rsqrtf(fmaxf(x, 1e-30f));
+    spc += x * r;  // |Fp| |Fc|
+    spp += pp;
+    scc += pc;
+    splp = fmaf(pc, __log2f(fmaxf(pc, 1.17549435e-38f)), splp);  // pc lg2 pc (0 at pc = 0)
     // normalised cross-power (migration.py:130-131)
-    const float inv = rcp_approx(m + 1e-12f);
-    return make_float2((fp.x * fc.x + fp.y * fc.y) * inv, (fp.y * fc.x - fp.x * fc.y) * inv);
+    return make_float2((fp.x * fc.x + fp.y * fc.y) * r, (fp.y * fc.x - fp.x * fc.y) * r);
   };
   const int k1a = lane >> 3, j1 = lane & 7;
   __syncwarp();  // every lane is done with the FFT scratch and the prev block
@@ -142,8 +147,8 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
           float2 c0, cn, p0, pn;
           unpack_dcny(v[h][j2], fetch(cur, km), c0, cn);
           unpack_dcny(pk, fetch(prev, km), p0, pn);
-          const float2 x0 = acc(1.f, p0, c0);
-          const float2 xn = acc(1.f, pn, cn);
+          const float2 x0 = acc(p0, c0);
+          const float2 xn = acc(pn, cn);
           v[h][j2] = make_float2(x0.x - xn.y, x0.y + xn.x);
         }
       }
@@ -156,16 +161,19 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float4 t = prev[(h * 4 + i) * 32 + lane];
-          v[h][2 * i] = acc(2.f, make_float2(t.x, t.y), v[h][2 * i]);
-          v[h][2 * i + 1] = acc(2.f, make_float2(t.z, t.w), v[h][2 * i + 1]);
+          v[h][2 * i] = acc(make_float2(t.x, t.y), v[h][2 * i]);
+          v[h][2 * i + 1] = acc(make_float2(t.z, t.w), v[h][2 * i + 1]);
         }
       }
     }
   }
   w448::inv<true>(v, a, slot, lane, tw);
-  // per-CTA partial sums: fp32 per lane, fp64 warp tree, warps in order
-  const double s0 = warp_sum_f64((double)spc), s1 = warp_sum_f64((double)spp);
-  const double s2 = warp_sum_f64((double)scc), s3 = warp_sum_f64((double)splp);
+  // per-CTA partial sums: fp32 per lane, fp64 warp tree, warps in order;
+  // the column's Hermitian weight and ln 2 applied here
+  const double wq = q == 0 ? 1.0 : 2.0;
+  const double s0 = wq * warp_sum_f64((double)spc), s1 = wq * warp_sum_f64((double)spp);
+  const double s2 = wq * warp_sum_f64((double)scc);
+  const double s3 = wq * 0.69314718055994530942 * warp_sum_f64((double)splp);
   if (lane == 0) {
     red[wid][0] = s0; red[wid][1] = s1; red[wid][2] = s2; red[wid][3] = s3;
   }
