@@ -13,7 +13,12 @@ oracle's own margin to the decision threshold is <= ``REL`` (1e-4 relative):
 * the gate, per step: |sim - tau| / tau;
 * psi within 1e-6 of 1 (fp32 cannot reproduce an fp64 1-ulp overshoot).
 
-Floats (sim, psi, alpha, energies) must agree within ``FTOL`` (1e-3) relative.
+Floats (sim, psi, alpha, energies) must agree within ``FTOL`` (1e-3) relative;
+energies additionally within the fp64 rounding floor of a patch energy,
+64 u P^2 s^2 (u = 2^-53, s = the frame's largest gray value, 1 for [0, 1]
+frames): both sides compute E as a difference of sums over P^2 squares, so a
+constant patch is ~1e-31 in the reference (DCT rounding) and ~1e-15 in the
+Parseval form, both numerically zero.
 """
 
 from __future__ import annotations
@@ -47,8 +52,9 @@ def _rel(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
-def compare(dev, ora: OracleDecision, cfg: OracleConfig, energies=None, rep=None):
-    """Check one step.  ``energies``: device per-token energies (optional)."""
+def compare(dev, ora: OracleDecision, cfg: OracleConfig, energies=None, rep=None, frame_scale=1.0):
+    """Check one step.  ``energies``: device per-token energies (optional);
+    ``frame_scale``: largest gray value of the frames (energy rounding floor)."""
     rep = rep or ParityReport()
     m = decision_margins(ora, cfg)
     n = ora.rows * ora.cols
@@ -64,6 +70,7 @@ def compare(dev, ora: OracleDecision, cfg: OracleConfig, energies=None, rep=None
     if energies is not None:
         e_ref = ora.energies
         floor = 1e-6 * float(e_ref.mean()) if e_ref.size else 0.0
+        floor = max(floor, 64.0 * 2.0 ** -53 * cfg.patch_size ** 2 * float(frame_scale) ** 2)
         err = np.abs(np.asarray(energies, dtype=np.float64) - e_ref)
         bad = err > FTOL * np.abs(e_ref) + floor
         if bad.any():

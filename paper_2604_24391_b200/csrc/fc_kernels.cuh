@@ -812,6 +812,12 @@ __global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config
       h.prev_const = cconst;
       h.steps += 1;
       kp.hdr[b] = h;
+    } else {
+      // the reference raises on a non-finite frame (frame.py:13-14); the
+      // spectrum state already holds this frame's (non-finite) transform, so
+      // the stream restarts cold: its next frame only re-establishes it
+      h.valid = 0;
+      kp.hdr[b] = h;
     }
   }
   __syncthreads();
