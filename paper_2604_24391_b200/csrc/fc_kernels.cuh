@@ -28,7 +28,7 @@
 
 #define FC_CB 8
 #define FC_THREADS 256
-#define FC_SEL_THREADS 512
+#define FC_SEL_THREADS 256
 #define FC_MAX_TOKENS 4096
 #define FC_MAX_PATCH 32
 
