@@ -236,7 +236,6 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
 
   // ---- phase 1: thread = columns (2t, 2t + 1)
   bool vary = false;
-  unsigned emax = 0u;
   double ref = 0.0;
   double s2[2] = {0.0, 0.0}, tu0[2] = {0.0, 0.0}, tu1[2] = {0.0, 0.0}, tu2[2] = {0.0, 0.0};
   float g32[14][2];
@@ -256,7 +255,6 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
       for (int c = 0; c < 2; ++c) {
         g32[xx][c] = (float)v[c];
         vary |= (v[c] != ref);
-        emax = max(emax, (unsigned)__double2hiint(v[c]) & 0x7ff00000u);
         s2[c] = fma(v[c], v[c], s2[c]);
         tu0[c] = fma(dc.c[0][xx], v[c], tu0[c]);
         tu1[c] = fma(dc.c[1][xx], v[c], tu1[c]);
@@ -265,7 +263,9 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
     }
   }
   const int anyvary = __syncthreads_or(vary);  // also: every pixel has been read
-  const int anybad = __syncthreads_or(emax == 0x7ff00000u);
+  // a NaN / Inf pixel makes its column's sum of squares non-finite (the
+  // squares of finite fp32-derived values cannot overflow fp64)
+  const int anybad = __syncthreads_or(!isfinite(s2[0]) || !isfinite(s2[1]));
   // fp32 gray as packed row pairs (2g, 2g+1), over the consumed stripe
 #pragma unroll
   for (int g = 0; g < 7; ++g)
