@@ -19,7 +19,9 @@ Two cached-step modes (``CachedEncoder.step``):
 * ``"subset"`` — the deployment-style reading: the cache holds final hidden
   states; recomputed tokens run the whole encoder attending among
   themselves, reused tokens take their (displacement-mapped) cached final
-  state.  Savings scale with the reuse ratio.
+  state.  The recomputed tokens of all streams are packed without padding
+  ([sum K_b, D] GEMMs, jagged-nested SDPA per stream), so the encoder work
+  scales with the recompute ratio.
 
 Both splice through ``fc_splice`` (bf16, bit copies) with the select's
 ``src_map``, and both report the cosine similarity of their output to a full
@@ -35,6 +37,11 @@ import torch
 import torch.nn.functional as F
 
 from .engine import FreqCacheEngine, splice, splice_packed
+
+try:  # variable-length attention for the packed subset mode (library kernel)
+    from flash_attn import flash_attn_varlen_func as _flash_varlen
+except Exception:  # noqa: BLE001 - optional dependency
+    _flash_varlen = None
 
 
 @dataclass(frozen=True)
@@ -81,6 +88,27 @@ class Block(torch.nn.Module):
     def forward(self, x, key_padding=None):
         y = self.ln1(x)
         x = x + self.attn(y, y, key_padding)
+        return x + self.fc2(F.gelu(self.fc1(self.ln2(x)), approximate="tanh"))
+
+    def forward_packed(self, x, offsets, max_len):
+        """Block over variable-length token sets packed as [T, D] (stream b's
+        tokens at rows offsets[b] .. offsets[b+1]); attention stays within a
+        stream: flash-attention varlen (library kernel) on [T, heads, hd],
+        or jagged nested tensors through SDPA where flash_attn is absent."""
+        y = self.ln1(x)
+        d = x.shape[-1]
+        hd = d // self.h
+        q, k, v = (t.unflatten(-1, (self.h, hd)) for t in
+                   F.linear(y, self.qkv.weight, self.qkv.bias).split(d, dim=-1))
+        if _flash_varlen is not None and x.dtype in (torch.float16, torch.bfloat16):
+            cu = offsets.to(torch.int32)
+            o = _flash_varlen(q.contiguous(), k.contiguous(), v.contiguous(), cu, cu, max_len, max_len)
+        else:
+            def nj(t):
+                return torch.nested.nested_tensor_from_jagged(t, offsets).transpose(1, 2)
+
+            o = F.scaled_dot_product_attention(nj(q), nj(k), nj(v)).transpose(1, 2).values()
+        x = x + self.proj(o.flatten(-2))
         return x + self.fc2(F.gelu(self.fc1(self.ln2(x)), approximate="tanh"))
 
     def forward_subset(self, xq, xkv):
@@ -172,27 +200,20 @@ class CachedEncoder:
                 x = blk(x)
             y = m.ln(x)
         else:
-            # streams sorted by recompute count and run in groups, each padded
-            # only to its own (128-bucketed) maximum; outputs are packed in
-            # stream order and spliced with per-stream offsets
+            # recomputed tokens of all streams packed stream-major (rec is
+            # front-packed per stream), no padding
             counts = valid.sum(dim=1)
             offsets = torch.zeros(B + 1, dtype=torch.int64, device=rec.device)
             offsets[1:] = torch.cumsum(counts, 0)
-            total = int(offsets[-1].item())
-            packed = torch.empty((max(total, 1), x0.shape[-1]), dtype=x0.dtype, device=x0.device)
-            cnt = counts.tolist()
-            order = sorted(range(B), key=lambda b: cnt[b])
-            for g0 in range(0, B, self.group):
-                grp = order[g0:g0 + self.group]
-                kg = min(rec.shape[1], max(128, -(-max(cnt[b] for b in grp) // 128) * 128))
-                gi = torch.tensor(grp, device=rec.device)
-                vg = valid[gi, :kg]
-                x = x0[gi, :kg]
+            x = x0[valid]                                   # [sum K_b, D]
+            if x.shape[0] == 0:
+                packed = x0.new_zeros((1, x0.shape[-1]))
+            else:
+                seg = torch.unique_consecutive(offsets)     # streams with no recomputed token drop out
+                max_len = int(counts.max().item())
                 for blk in m.blocks:
-                    x = blk(x, key_padding=vg)
-                yg = m.ln(x)
-                pos = offsets[gi][:, None] + torch.arange(kg, device=rec.device)[None, :]
-                packed[pos[vg]] = yg[vg]
+                    x = blk.forward_packed(x, seg, max_len)
+                packed = m.ln(x)
             splice_packed(out.src_map, self.h1[i], self.ages[i], packed, offsets[:B].contiguous(),
                           self.h1[o], self.ages[o])
             y = self.h1[o]

@@ -18,6 +18,8 @@ from paper_2604_24391_b200.vit import CachedEncoder, ViT, ViTConfig, cosine
 
 S = int(os.environ.get("STREAMS", 16))
 T = int(os.environ.get("STEPS", 48))
+GROUP = int(os.environ.get("GROUP", 0))  # subset mode: streams per padded group (0 = all)
+MODES = os.environ.get("MODES", "layer1,subset").split(",")
 dev = torch.device("cuda")
 c = ViTConfig()
 model = ViT(c).to(dev, torch.bfloat16).eval()
@@ -25,7 +27,7 @@ frames = torch_stream_frames(S, T, c.image, c.image, seed=1000, device=dev)  # [
 cfg = CacheConfig(patch_size=c.patch)
 ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-res = {"config": {"streams": S, "steps": T, "vit": c.__dict__, "dtype": "bf16"}}
+res = {"config": {"streams": S, "steps": T, "vit": c.__dict__, "dtype": "bf16", "subset_group": GROUP or S}}
 with torch.no_grad():
     for _ in range(2):
         model(frames[0])
@@ -36,13 +38,13 @@ with torch.no_grad():
     e1.record()
     torch.cuda.synchronize()
     res["full_ms_per_step"] = e0.elapsed_time(e1) / T
-    for mode in ("layer1", "subset"):
-        enc = CachedEncoder(model, S, mode=mode)
+    for mode in MODES:
+        enc = CachedEncoder(model, S, mode=mode, group=GROUP)
         enc.step(frames[0], cfg)  # cold start (full compute)
         torch.cuda.synchronize()
         for t in range(1, 4):  # warm the recompute-bucket shapes
             enc.step(frames[t], cfg)
-        enc = CachedEncoder(model, S, mode=mode)
+        enc = CachedEncoder(model, S, mode=mode, group=GROUP)
         enc.step(frames[0], cfg)
         torch.cuda.synchronize()
         cos, reuse, evs = [], [], []
