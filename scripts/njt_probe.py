@@ -46,3 +46,23 @@ try:
     print("flashinfer", flashinfer.__version__)
 except Exception as e:  # noqa: BLE001
     print("flashinfer import failed", e)
+try:
+    import torch.nn.attention as A
+    print("flash impls", A.list_flash_attention_impls(), "current", A.current_flash_attention_impl())
+except Exception as e:  # noqa: BLE001
+    print("impl list failed", e)
+try:
+    from torch.nn.attention.varlen import varlen_attn
+    mx = int(lens.max())
+    print("torch varlen ms", bench(lambda: varlen_attn(q, k, v, off, off, mx, mx)))
+except Exception as e:  # noqa: BLE001
+    print("torch varlen failed:", type(e).__name__, str(e)[:300])
+try:
+    import torch.nn.attention as A
+    A.activate_flash_attention_impl("FA4")
+    print("FA4 active", A.current_flash_attention_impl())
+    print("dense sdpa FA4 ms", bench(lambda: F.scaled_dot_product_attention(qd, qd, qd)))
+    from torch.nn.attention.varlen import varlen_attn
+    print("torch varlen FA4 ms", bench(lambda: varlen_attn(q, k, v, off, off, mx, mx)))
+except Exception as e:  # noqa: BLE001
+    print("FA4 failed:", type(e).__name__, str(e)[:300])
