@@ -215,10 +215,18 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FC_BENCH_DEVICE / FC_DIST_BACKEND: plumbing checks of the multi-rank
+    # path on a one-GPU box (ranks share the device over gloo; not a scaling
+    # measurement — the driver's runs use one GPU per rank over NCCL)
+    local = int(os.environ.get("FC_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("FC_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2604_24391_b200 import CacheConfig, FreqCacheEngine, SpliceState
     from paper_2604_24391_b200.synth import torch_stream_frames
@@ -516,7 +524,8 @@ def run_ours(a):
             "config": {"workload": "config5 per GPU: select + splice, adaptive budget, refresh on shift>1",
                        "streams_per_gpu": S, "size": H, "channels": 3, "patch": P, "tokens": N,
                        "hidden": D, "hidden_dtype": "bf16", "frame_ring_steps": R,
-                       "l2": "inputs > L2 (1.23 GB of frames per step, 29.6 GB ring)"},
+                       "l2": f"inputs > L2 ({S * H * H * 12 / 1e9:.2f} GB of frames per step, "
+                             f"{R * S * H * H * 12 / 1e9:.1f} GB ring)"},
             "tokens_per_s": value * N,
             "roofline": roofline, "roofline_step": roofline_step, "kernels": kernels,
             "cpu_baseline": cpu,
