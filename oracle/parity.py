@@ -23,7 +23,6 @@ Parseval form, both numerically zero.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass, field
 
 import numpy as np

@@ -14,7 +14,6 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
-import numpy as np
 import torch
 
 from . import _native as nat

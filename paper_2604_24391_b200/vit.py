@@ -30,7 +30,6 @@ recompute of the same frame.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import torch

@@ -1,5 +1,5 @@
 """Diagnostics: device time of select only / splice only / both (512 streams, 448^2)."""
-import os, sys, time
+import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2604_24391_b200 import CacheConfig, FreqCacheEngine, splice

@@ -9,7 +9,6 @@ pool over streams.
 import multiprocessing as mp
 import os
 
-import numpy as np
 import pytest
 
 from oracle import freqcache_oracle as O
