@@ -65,3 +65,38 @@ def test_fast_path_degenerate_and_nonfinite_streams(cuda):
             if (t, s) == (2, 6):
                 assert d.displacement.di == 0 and d.displacement.dj == 0 and d.sim_freq == pytest.approx(1.0)
     assert rep.ok, rep.errors
+
+
+def test_fast_path_formats_agree(cuda):
+    """448 x 448: the same frames as RGB fp32, as their fp64 luma and as
+    fp32 gray give the decisions the oracle gives for the same gray values;
+    RGB fp32 and its exact fp64 luma give bitwise-identical energies."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.api import decision_from_device
+    from paper_2604_24391_b200.synth import stream_frames
+    S, T = 2, 4
+    rgb = np.stack([stream_frames(4200, s, T, H, H) for s in range(S)], axis=1)       # T, S, H, W, 3 fp32
+    r, g, b = (rgb[..., i].astype(np.float64) for i in range(3))
+    g64 = (0.299 * r + 0.587 * g) + 0.114 * b
+    g32 = g64.astype(np.float32)
+    cfg = fc.CacheConfig(patch_size=P)
+    oc = O.OracleConfig(patch_size=P)
+    outs = {}
+    for name, fmt, fr in (("rgb", "rgb", rgb), ("gray64", "gray64", g64), ("gray32", "gray32", g32)):
+        eng = fc.FreqCacheEngine(S, H, H, P, fmt=fmt)
+        outs[name] = []
+        for t in range(T):
+            o = eng.select(torch.from_numpy(np.ascontiguousarray(fr[t])).cuda(), cfg)
+            outs[name].append((o.host_results(), o.reuse_idx.cpu().numpy(), o.recompute_idx.cpu().numpy(),
+                               o.refresh_mask.cpu().numpy(), o.energy.cpu().numpy()))
+    rep = ParityReport()
+    for t in range(1, T):
+        assert np.array_equal(outs["rgb"][t][4], outs["gray64"][t][4])  # identical fp64 luma -> energies
+        for name, ref in (("rgb", g64), ("gray64", g64), ("gray32", g32.astype(np.float64))):
+            res, ri, rc, rm, en = outs[name][t]
+            for s in range(S):
+                d = decision_from_device(res[s], ri[s], rc[s], rm[s], step=t)
+                o = O.decide(ref[t - 1, s], ref[t, s], oc, step=t)
+                compare(d, o, oc, energies=en[s], rep=rep)
+    assert rep.ok, rep.errors
