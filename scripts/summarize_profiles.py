@@ -79,8 +79,8 @@ def main(tag):
     for k, v in sorted(per.items(), key=lambda x: -sum(x[1])):
         lines.append(f"| {k} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {100 * sum(v) / tot:.1f} % |")
     lines += ["", "## Full capture (`--set full`), one launch per kernel at the bench configuration", "",
-              "| kernel | us | DRAM read MB | DRAM write MB | warp-inst (M) | issue active % | warps active % | top stalls |",
-              "|---|---|---|---|---|---|---|---|"]
+              "| kernel | us | DRAM read MB | DRAM write MB | warp-inst (M) | issue active % | warps active % | FMA pipe % | FP64 pipe % | tensor pipe % | top stalls |",
+              "|---|---|---|---|---|---|---|---|---|---|---|"]
     for d in rd:
         k = short(g(d, "Kernel Name"))
         rdb = float(g(d, "dram__bytes_read.sum") or 0)
@@ -98,6 +98,9 @@ def main(tag):
                      f"{wrb * scale / 1e6:.1f} | {float(g(d, 'smsp__inst_executed.sum')) / 1e6:.2f} | "
                      f"{float(g(d, 'smsp__issue_active.avg.pct_of_peak_sustained_active')):.1f} | "
                      f"{float(g(d, 'sm__warps_active.avg.pct_of_peak_sustained_active')):.1f} | "
+                     f"{float(g(d, 'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
+                     f"{float(g(d, 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
+                     f"{float(g(d, 'TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed') or 0):.1f} | "
                      + ", ".join(f"{h} {v:.2f}" for h, v in st) + " |")
     lines += ["", "## Per-kernel timing inside bench.py (CUDA events, serialised pass)", "",
               "| kernel | ms | share | interface bytes | GB/s |", "|---|---|---|---|---|"]
