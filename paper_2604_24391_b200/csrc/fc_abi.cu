@@ -542,12 +542,14 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // Bulk (TMA) copier unless disabled (FC_SPLICE_BULK=0) or the rows/batch do
   // not fit its shared-memory slots.
-  static const int NL = env_int("FC_SPLICE_BULK_NL", 8, 2, 16);
+  // lanes per copier CTA: the compiled variants are 2, 4, 8 and 16
+  static const int NLreq = env_int("FC_SPLICE_BULK_NL", 8, 2, 16);
+  static const int NL = NLreq <= 2 ? 2 : NLreq <= 4 ? 4 : NLreq <= 8 ? 8 : 16;
   const size_t bulk_smem = (size_t)NL * 2 * row_bytes + (size_t)(batch + 1) * 4;
   static const int use_bulk = env_int("FC_SPLICE_BULK", 1, 0, 1);
   if (use_bulk && bulk_smem <= 96 * 1024) {
     static const int per_sm = env_int("FC_SPLICE_BULK_CTAS", 2, 1, 32);
-    auto fn = NL <= 2 ? k_splice_ip_bulk<2> : NL <= 4 ? k_splice_ip_bulk<4> : NL <= 8 ? k_splice_ip_bulk<8>
+    auto fn = NL == 2 ? k_splice_ip_bulk<2> : NL == 4 ? k_splice_ip_bulk<4> : NL == 8 ? k_splice_ip_bulk<8>
                                                                                     : k_splice_ip_bulk<16>;
     if (bulk_smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem);
     fn<<<sms * per_sm, 32, bulk_smem, st>>>(
