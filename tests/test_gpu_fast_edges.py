@@ -100,3 +100,39 @@ def test_fast_path_formats_agree(cuda):
                 o = O.decide(ref[t - 1, s], ref[t, s], oc, step=t)
                 compare(d, o, oc, energies=en[s], rep=rep)
     assert rep.ok, rep.errors
+
+
+@pytest.mark.parametrize("h,w,p", [(1008, 1008, 16), (1344, 448, 28), (448, 224, 14), (1536, 1536, 24)])
+def test_generic_path_envelope(cuda, h, w, p):
+    """Near the generic kernels' envelope (N <= 4096, P <= 32, the row pass's
+    shared memory ~ 12 P W bytes <= 227 KB): 1008^2 / P 16 (N = 3969), a tall
+    1344 x 448 / P 28 frame and a rectangular 448 x 224 frame, two streams
+    against the oracle; 1536^2 / P 24 is outside (shared memory) and refused
+    at plan creation."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200._native import NativeError
+    from paper_2604_24391_b200.api import decision_from_device
+    if (h, w, p) == (1536, 1536, 24):
+        with pytest.raises(NativeError, match="envelope"):
+            fc.FreqCacheEngine(1, h, w, p, fmt="gray64")
+        return
+    rng = np.random.default_rng(h + w + p)
+    base = rng.random((h, w))
+    fr = np.stack([np.stack([np.roll(base, (3 * t + s, 2 * t), axis=(0, 1)) for s in range(2)]) for t in range(3)])
+    eng = fc.FreqCacheEngine(2, h, w, p, fmt="gray64")
+    cfg = fc.CacheConfig(patch_size=p)
+    oc = O.OracleConfig(patch_size=p)
+    rep = ParityReport()
+    for t in range(3):
+        out = eng.select(torch.from_numpy(np.ascontiguousarray(fr[t])).cuda(), cfg)
+        if t == 0:
+            continue
+        res = out.host_results()
+        ri, rc, rm = out.reuse_idx.cpu().numpy(), out.recompute_idx.cpu().numpy(), out.refresh_mask.cpu().numpy()
+        en = out.energy.cpu().numpy()
+        for s in range(2):
+            d = decision_from_device(res[s], ri[s], rc[s], rm[s], step=t)
+            o = O.decide(fr[t - 1, s], fr[t, s], oc, step=t)
+            compare(d, o, oc, energies=en[s], rep=rep)
+    assert rep.ok, rep.errors
