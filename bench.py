@@ -43,7 +43,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--streams", type=int, default=512, help="streams per rank")
+    ap.add_argument("--streams", type=int, default=512,
+                    help="streams per rank (weak scaling, default); with --strong: streams of the whole job")
+    ap.add_argument("--strong", action="store_true",
+                    help="config 5 read literally: --streams in total, sharded across the ranks")
     ap.add_argument("--size", type=int, default=448)
     ap.add_argument("--patch", type=int, default=14)
     ap.add_argument("--dim", type=int, default=1152)
@@ -231,13 +234,15 @@ def run_ours(a):
     from paper_2604_24391_b200.synth import torch_stream_frames
 
     S, H, P, D, R = a.streams, a.size, a.patch, a.dim, a.ring
+    total_streams = S if a.strong else S * world
     N = (H // P) ** 2
     cfg = CacheConfig(patch_size=P)
 
     # ---- inputs, resident in HBM before timing (untimed generation); this
     # rank's streams are its contiguous block of the job's S * world streams
     from paper_2604_24391_b200.dist import gather_counters, shard, step_counters
-    lo, hi = shard(S * world, world, rank)
+    lo, hi = shard(total_streams, world, rank)
+    S = hi - lo
     frames = torch.empty((R, S, H, H, 3), dtype=torch.float32, device=dev)
     chunk = 64
     for c0 in range(0, S, chunk):
@@ -342,7 +347,7 @@ def run_ours(a):
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
-    frames_total = S * a.steps * world
+    frames_total = total_streams * a.steps
     value = frames_total / (ms / 1e3)
 
     # decision statistics of the last timed step over all ranks (the only
@@ -446,9 +451,9 @@ def run_ours(a):
     ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-    e2e_val = S * ke * world / (float(ems.item()) / 1e3)
-    h2d = S * H * H * 3 * 4
-    d2h = S * 136 + S * N * 4
+    e2e_val = total_streams * ke / (float(ems.item()) / 1e3)
+    h2d = total_streams * H * H * 3 * 4          # whole job, per step
+    d2h = total_streams * 136 + total_streams * N * 4
     # the link the e2e number is bound by: plain pinned H2D copy of one step's frames
     for _ in range(2):
         stages[0].copy_(host[0], non_blocking=True)
@@ -459,8 +464,8 @@ def run_ours(a):
         stages[i & 1].copy_(host[i % HR], non_blocking=True)
     p1.record(stream)
     torch.cuda.synchronize()
-    pcie_gbs = 3 * h2d / (p0.elapsed_time(p1) / 1e3) / 1e9
-    e2e_h2d_gbs = h2d * e2e_val / S / world / 1e9
+    pcie_gbs = 3 * S * H * H * 3 * 4 / (p0.elapsed_time(p1) / 1e3) / 1e9
+    e2e_h2d_gbs = S * H * H * 3 * 4 * e2e_val / total_streams / 1e9   # per rank (its own PCIe link)
 
     # ---- single-stream step latency (select + splice), CUDA-graph replay:
     # config 1 (224x224, fixed 50 % budget) and one config-2 stream (448x448)
@@ -517,11 +522,12 @@ def run_ours(a):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "strong" if a.strong else "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (frozen generator, torch draw on GPU; cache/fresh bf16 N(0,1))",
             "config": {"workload": "config5 per GPU: select + splice, adaptive budget, refresh on shift>1",
-                       "streams_per_gpu": S, "size": H, "channels": 3, "patch": P, "tokens": N,
+                       "streams_per_gpu": S, "streams_total": total_streams, "size": H, "channels": 3, "patch": P, "tokens": N,
                        "hidden": D, "hidden_dtype": "bf16", "frame_ring_steps": R,
                        "l2": f"inputs > L2 ({S * H * H * 12 / 1e9:.2f} GB of frames per step, "
                              f"{R * S * H * H * 12 / 1e9:.1f} GB ring)"},
