@@ -56,7 +56,8 @@ def test_random_shift_pairs(cuda, shape, p):
 
 
 def test_reference_buckets(cuda):
-    """The reference's decide/decide_reference buckets (test_acceptance.py:156-204)."""
+    """The reference's decide/decide_reference buckets, 1,000 instances as in its
+    acceptance criterion 6 (test_acceptance.py:156-204)."""
     import paper_2604_24391_b200 as fc
     rng = np.random.default_rng(600)
     cfgs = {
@@ -66,7 +67,7 @@ def test_reference_buckets(cuda):
     }
     rep = ParityReport()
     seen = {"flush": 0, "empty": 0, "capped": 0}
-    for i in range(200):
+    for i in range(1000):
         bucket = i % 5
         prev = rng.random((32, 32))
         if bucket == 0:
@@ -98,7 +99,7 @@ def test_reference_buckets(cuda):
         seen["flush"] += d.flushed
         seen["empty"] += d.k_candidate == 0 and not d.flushed
         seen["capped"] += 0 < d.k_final == d.k_reuse < d.k_candidate
-    assert seen["flush"] >= 40 and seen["empty"] >= 40 and seen["capped"] >= 30
+    assert seen["flush"] >= 200 and seen["empty"] >= 200 and seen["capped"] >= 150
 
 
 def test_tied_energies_order(cuda):
