@@ -320,3 +320,30 @@ def test_config2_sweep_16_streams(cuda):
             n_exact += tuple(d.reuse_set) == o.reuse_set and tuple(d.refresh_set) == o.refresh_set
     assert rep.ok, rep.errors
     print(f"config-2 sweep: {n_exact}/{S * (T - 1)} decisions identical to the oracle; exemptions {rep.exemptions}")
+
+
+def test_acceptance_shift_recovery_and_latency(cuda):
+    """The reference's acceptance criteria 3 and 9 through the façade: exact
+    recovery of 100/100 random cyclic shifts, and decide() median under
+    10 ms at 224x224 / P16."""
+    import time
+    import paper_2604_24391_b200 as fc
+    c, _ = _cfg(patch_size=16)
+    rng = np.random.default_rng(909)
+    ok = 0
+    for _ in range(100):
+        prev = rng.random((64, 64))
+        sh = (int(rng.integers(-31, 32)), int(rng.integers(-31, 32)))
+        d = fc.decide(prev, np.roll(prev, sh, axis=(0, 1)), c)
+        ok += (d.displacement.di, d.displacement.dj) == sh
+    assert ok == 100
+    a, b = rng.random((224, 224)), rng.random((224, 224))
+    fc.decide(a, b, c)
+    times = []
+    for _ in range(21):
+        t0 = time.perf_counter()
+        fc.decide(a, b, c)
+        times.append(time.perf_counter() - t0)
+    med = sorted(times)[10]
+    print(f"facade decide 224x224/P16 median {med * 1e3:.3f} ms")
+    assert med < 10e-3
