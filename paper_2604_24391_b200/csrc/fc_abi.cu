@@ -545,12 +545,15 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
   // lanes per copier CTA: the compiled variants are 2, 4, 8 and 16
   static const int NLreq = env_int("FC_SPLICE_BULK_NL", 8, 2, 16);
   static const int NL = NLreq <= 2 ? 2 : NLreq <= 4 ? 4 : NLreq <= 8 ? 8 : 16;
-  const size_t bulk_smem = (size_t)NL * 2 * row_bytes + (size_t)(batch + 1) * 4;
+  static const int SL = env_int("FC_SPLICE_BULK_SLOTS", 2, 2, 4);
+  const size_t bulk_smem = (size_t)NL * SL * row_bytes + (size_t)(batch + 1) * 4;
   static const int use_bulk = env_int("FC_SPLICE_BULK", 1, 0, 1);
   if (use_bulk && bulk_smem <= 96 * 1024) {
     static const int per_sm = env_int("FC_SPLICE_BULK_CTAS", 2, 1, 32);
-    auto fn = NL == 2 ? k_splice_ip_bulk<2> : NL == 4 ? k_splice_ip_bulk<4> : NL == 8 ? k_splice_ip_bulk<8>
-                                                                                    : k_splice_ip_bulk<16>;
+    auto fn = SL == 3 ? (NL == 4 ? k_splice_ip_bulk<4, 3> : NL == 8 ? k_splice_ip_bulk<8, 3> : k_splice_ip_bulk<16, 3>)
+            : SL == 4 ? (NL == 4 ? k_splice_ip_bulk<4, 4> : NL == 8 ? k_splice_ip_bulk<8, 4> : k_splice_ip_bulk<16, 4>)
+            : NL == 2 ? k_splice_ip_bulk<2> : NL == 4 ? k_splice_ip_bulk<4> : NL == 8 ? k_splice_ip_bulk<8>
+                                                                                 : k_splice_ip_bulk<16>;
     if (bulk_smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem);
     fn<<<sms * per_sm, 32, bulk_smem, st>>>(
         batch, n_tokens, (int)row_bytes, src_map, reinterpret_cast<char*>(cache0), reinterpret_cast<char*>(cache1),

@@ -1189,13 +1189,17 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice_ip(int total, int n_token
 }
 
 // Bulk-copy variant of k_splice_ip for running beside the select kernels:
-// one warp per CTA, NL lanes each own two row slots in shared memory and
+// one warp per CTA, NL lanes each own SL row slots in shared memory and
 // move rows with the TMA engine (global -> shared -> global), so a CTA keeps
-// 2 * NL rows in flight while issuing a handful of instructions per row.
+// SL * NL rows in flight while issuing a handful of instructions per row
+// (a slot is refilled once its store from SL - 1 rows back has been read).
 // Rows are claimed dynamically (one atomic per row) so CTAs that start late,
 // behind a resident select kernel, simply take less work.  Task t maps to
 // (stream, k) through an exclusive scan of counts[] built per CTA.
-template <int NL>
+#ifndef FC_SPLICE_CLAIM
+#define FC_SPLICE_CLAIM 8
+#endif
+template <int NL, int SL = 2>
 __global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, int row_bytes,
                                                        const int32_t* __restrict__ src_map, char* cache0,
                                                        char* cache1, int64_t* ages0, int64_t* ages1,
@@ -1203,11 +1207,11 @@ __global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, 
                                                        const uint8_t* __restrict__ slot_out,
                                                        const int32_t* __restrict__ rows, int32_t* counts,
                                                        const char* __restrict__ fresh, int compact, int fresh_rows) {
-  extern __shared__ __align__(128) unsigned char smem[];  // [NL][2][row_bytes] | offs[batch + 1]
-  __shared__ __align__(8) uint64_t bar[NL * 2];
+  extern __shared__ __align__(128) unsigned char smem[];  // [NL][SL][row_bytes] | offs[batch + 1]
+  __shared__ __align__(8) uint64_t bar[NL * SL];
   const int lane = threadIdx.x;
-  int* offs = reinterpret_cast<int*>(smem + (size_t)NL * 2 * row_bytes);
-  if (lane < NL * 2) tma::bar_init(&bar[lane], 1);
+  int* offs = reinterpret_cast<int*>(smem + (size_t)NL * SL * row_bytes);
+  if (lane < NL * SL) tma::bar_init(&bar[lane], 1);
   // exclusive scan of counts (lane-contiguous segments)
   const int per = (batch + 31) / 32, q0 = lane * per, q1 = min(batch, q0 + per);
   int sum = 0;
@@ -1225,15 +1229,25 @@ __global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, 
   __syncwarp();
   if (lane >= NL) return;
   int* work = counts + batch;
-  unsigned char* slot0 = smem + (size_t)lane * 2 * row_bytes;
+  unsigned char* slot0 = smem + (size_t)lane * SL * row_bytes;
   bool pend = false;
   char* pdst = nullptr;
   int pslot = 0;
   uint32_t pphase = 0;
+  // rows are claimed G at a time per lane: the single work counter serves
+  // about one atomic per L2 cycle, which bounded the copier when it claimed
+  // one row per atomic
+  constexpr int G = FC_SPLICE_CLAIM;
+  int claim = 0, left = 0;
   for (int it = 0;; ++it) {
-    const int task = atomicAdd(work, 1);
+    if (left == 0) {
+      claim = atomicAdd(work, G);
+      left = G;
+    }
+    const int task = claim + (G - left);
+    --left;
     const bool have = task < tot;
-    const int sl = it & 1;
+    const int sl = it % SL;
     unsigned char* buf = slot0 + sl * row_bytes;
     char* dst = nullptr;
     if (have) {
@@ -1256,20 +1270,22 @@ __global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, 
       const int64_t* cage = cur ? ages1 : ages0;
       int64_t* nage = nxt ? ages1 : ages0;
       nage[base + p] = s >= 0 ? cage[base + s] + 1 : 0;
-      // this slot's previous store (two rows back) must have left shared memory
-      tma::bulk_wait_read0();
-      tma::bar_expect(&bar[lane * 2 + sl], row_bytes);
-      tma::bulk_g2s(buf, src, row_bytes, &bar[lane * 2 + sl]);
+      // this slot's previous store (SL rows back) must have left shared
+      // memory; the SL - 2 stores issued after it may still be reading
+      if constexpr (SL == 2) tma::bulk_wait_read0();
+      else asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(SL - 2) : "memory");
+      tma::bar_expect(&bar[lane * SL + sl], row_bytes);
+      tma::bulk_g2s(buf, src, row_bytes, &bar[lane * SL + sl]);
     }
     if (pend) {
-      tma::bar_wait(&bar[lane * 2 + pslot], pphase);
+      tma::bar_wait(&bar[lane * SL + pslot], pphase);
       tma::bulk_s2g(pdst, slot0 + pslot * row_bytes, row_bytes);
     }
     if (!have) break;
     pend = true;
     pdst = dst;
     pslot = sl;
-    pphase = (it >> 1) & 1;
+    pphase = (it / SL) & 1;
   }
   tma::bulk_wait0();
 }
