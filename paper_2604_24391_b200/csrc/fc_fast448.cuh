@@ -1,158 +1,11 @@
 // Fast path for the BASELINE geometry (448 x 448 frames, P = 14, N = 1024):
-// register-resident 448-point FFTs with compile-time thread roles.
-//
-// 448 = 7 * 64, 64 = 8 * 8.  Forward (natural order in, permuted out):
-//   stage 1  role n2 in [0,64): A[n2][k1] = DFT7_{n1}(x[64 n1 + n2]) * w448^{n2 k1}
-//   stage 2  role (k1, m2):     B[k1][m2][j1] = DFT8_{m1}(A[8 m1 + m2][k1])
-//   stage 3  role (k1, j1):     X[k1 + 7 j1 + 56 j2] = DFT8_{m2}(B[k1][m2][j1] * w64^{m2 j1})
-// so role r < 56 ends holding X[k1 + 7 j1 + 56 j2], j2 = 0..7, (k1, j1) = (r/8, r%8).
-// The inverse runs the same stages transposed (permuted in, natural out) with
-// conjugate twiddles, so a forward->pointwise->inverse chain never reorders.
-// Exchanges go through shared memory in layouts chosen to be bank-conflict
-// free for 8-byte accesses: S1[k1][n2] and S2[k1][j1][m2] with row stride 72
-// and j1 stride 9 (k1 rows of two neighbouring roles land 16 banks apart).
-// Kernels whose transforms interleave c-fastest (column pass) use a per-
-// transform scratch stride of 514 (= 2 mod 16) so the 8 transforms of a
-// half-warp spread over disjoint 4-bank groups.
+// K_A, the row pass (stripe luma + block-DCT energies + packed-pair row
+// FFTs).  The 448-point FFT itself (7 x 8 x 8, one transform per warp) is
+// in fc_wfft448.cuh; K_B / K_C are in fc_fast448w.cuh.
 #pragma once
 #include "fc_fft.cuh"
 #include "fc_tma.cuh"
 #include "fc_wfft448.cuh"
-
-namespace f448 {
-
-constexpr int N = 448;
-constexpr int XR = 504;  // exchange scratch per transform, role-fastest mapping
-constexpr int XC = 514;  // exchange scratch per transform, transform-fastest mapping
-
-__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
-
-template <bool INV>
-__device__ __forceinline__ float2 twid(const float2* __restrict__ t, int i) {
-  const float2 w = __ldg(t + i);
-  return INV ? conjf2(w) : w;
-}
-
-// Per-role twiddles, loaded once per thread (ahead of the data they scale):
-// w1[k1-1] = w448^{r k1}, w3[m2-1] = w64^{m2 (r & 7)}.
-struct Tw {
-  float2 w1_[6];
-  float2 w3_[7];
-  __device__ __forceinline__ float2 w1(int k1) const { return w1_[k1 - 1]; }
-  __device__ __forceinline__ float2 w3(int m2) const { return w3_[m2 - 1]; }
-};
-
-// Twiddles read at their point of use (fewer live registers).
-struct TwLazy {
-  const float2* __restrict__ t448;
-  const float2* __restrict__ t64;
-  int r;
-  __device__ __forceinline__ float2 w1(int k1) const { return __ldg(t448 + (k1 - 1) * 64 + r); }
-  __device__ __forceinline__ float2 w3(int m2) const { return __ldg(t64 + (m2 - 1) * 8 + (r & 7)); }
-};
-
-__device__ __forceinline__ void load_tw(Tw& tw, int r, const float2* __restrict__ tw448,
-                                        const float2* __restrict__ tw64) {
-#pragma unroll
-  for (int k1 = 1; k1 < 7; ++k1) tw.w1_[k1 - 1] = __ldg(tw448 + (k1 - 1) * 64 + r);
-#pragma unroll
-  for (int m2 = 1; m2 < 8; ++m2) tw.w3_[m2 - 1] = __ldg(tw64 + (m2 - 1) * 8 + (r & 7));
-}
-
-template <bool INV>
-__device__ __forceinline__ float2 tw_apply(float2 v, float2 w) {
-  return cmul(v, INV ? conjf2(w) : w);
-}
-
-// Forward-ordered FFT.  a[n1] = x[64 n1 + r] on entry (all 64 roles).  On
-// exit roles r < 56 hold X[k1 + 7 j1 + 56 j2] in b[j2].  S: this transform's
-// scratch.  Contains three __syncthreads (every thread must call).
-template <bool INV, class TW>
-__device__ __forceinline__ void fwd(float2 (&a)[7], float2 (&b)[8], float2* S, int r, const TW& tw) {
-  DftOdd<7, INV>::run(a);
-#pragma unroll
-  for (int k1 = 1; k1 < 7; ++k1) a[k1] = tw_apply<INV>(a[k1], tw.w1(k1));
-#pragma unroll
-  for (int k1 = 0; k1 < 7; ++k1) S[k1 * 72 + r] = a[k1];
-  __syncthreads();
-  const bool act = r < 56;
-  const int k1 = r >> 3, lo = r & 7;
-  if (act) {
-#pragma unroll
-    for (int m1 = 0; m1 < 8; ++m1) b[m1] = S[k1 * 72 + 8 * m1 + lo];
-  }
-  __syncthreads();
-  if (act) {
-    Dft<8, INV>::run(b);
-#pragma unroll
-    for (int j1 = 0; j1 < 8; ++j1) S[k1 * 72 + 9 * j1 + lo] = b[j1];
-  }
-  __syncthreads();
-  if (act) {
-#pragma unroll
-    for (int m2 = 0; m2 < 8; ++m2) b[m2] = S[k1 * 72 + 9 * lo + m2];
-#pragma unroll
-    for (int m2 = 1; m2 < 8; ++m2) b[m2] = tw_apply<INV>(b[m2], tw.w3(m2));
-    Dft<8, INV>::run(b);
-  }
-}
-
-// Transposed FFT: roles r < 56 hold X[k1 + 7 j1 + 56 j2] in b[j2] on entry;
-// on exit a[n1] = x[64 n1 + r] for all 64 roles.  Three __syncthreads.
-template <bool INV, class TW>
-__device__ __forceinline__ void inv(float2 (&b)[8], float2 (&a)[7], float2* S, int r, const TW& tw) {
-  const bool act = r < 56;
-  const int k1 = r >> 3, lo = r & 7;
-  if (act) {
-    Dft<8, INV>::run(b);  // over j2 -> m2
-#pragma unroll
-    for (int m2 = 1; m2 < 8; ++m2) b[m2] = tw_apply<INV>(b[m2], tw.w3(m2));
-#pragma unroll
-    for (int m2 = 0; m2 < 8; ++m2) S[k1 * 72 + 9 * lo + m2] = b[m2];
-  }
-  __syncthreads();
-  if (act) {
-#pragma unroll
-    for (int j1 = 0; j1 < 8; ++j1) b[j1] = S[k1 * 72 + 9 * j1 + lo];
-  }
-  __syncthreads();
-  if (act) {
-    Dft<8, INV>::run(b);  // over j1 -> m1
-#pragma unroll
-    for (int m1 = 0; m1 < 8; ++m1) S[k1 * 72 + 8 * m1 + lo] = b[m1];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 7; ++q) a[q] = S[q * 72 + r];
-#pragma unroll
-  for (int q = 1; q < 7; ++q) a[q] = tw_apply<INV>(a[q], tw.w1(q));
-  DftOdd<7, INV>::run(a);  // over k1 -> n1
-}
-
-}  // namespace f448
-
-__device__ __forceinline__ float sqrt_approx(float x) {
-  float y;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-template <bool LAZY> struct TwSel;
-template <> struct TwSel<true> {
-  __device__ __forceinline__ static f448::TwLazy make(const KParams& kp, int r) { return {kp.tw448, kp.tw64, r}; }
-};
-template <> struct TwSel<false> {
-  __device__ __forceinline__ static f448::Tw make(const KParams& kp, int r) {
-    f448::Tw t;
-    f448::load_tw(t, r, kp.tw448, kp.tw64);
-    return t;
-  }
-};
 
 struct Dct14 {
   double c[3][14];  // orthonormal DCT-II rows u < 3 for P = 14

@@ -1,5 +1,5 @@
-// K_B and K_C of the 448 x 448 fast path (K_A, the geometry and the f448
-// CTA-wide FFT are in fc_fast448.cuh).
+// K_B and K_C of the 448 x 448 fast path (K_A is in fc_fast448.cuh, the
+// warp-owned 448-point FFT in fc_wfft448.cuh).
 //
 // Both kernels are warp-owned: every 448-point transform belongs to one warp
 // (w448 in fc_wfft448.cuh), every warp stages its own tiles with its own TMA

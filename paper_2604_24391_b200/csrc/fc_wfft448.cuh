@@ -1,10 +1,16 @@
 // Warp-owned 448-point FFTs: one warp runs one whole transform, so the data
 // exchanges between radix stages need only __syncwarp, never a CTA barrier.
 //
-// Same 7 x 8 x 8 factorisation and shared-memory layouts as f448 (see
-// fc_fast448.cuh), with the 64 thread roles of a transform folded onto the
-// 32 lanes of one warp: lane l plays roles r = l and r = l + 32 ("halves"
-// h = 0, 1).  Radix-8 stages have 56 groups; half 1 is active on lanes < 24.
+// 448 = 7 * 64, 64 = 8 * 8.  Forward (natural order in, permuted out):
+//   stage 1  role n2 in [0,64): A[n2][k1] = DFT7_{n1}(x[64 n1 + n2]) * w448^{n2 k1}
+//   stage 2  role (k1, m2):     B[k1][m2][j1] = DFT8_{m1}(A[8 m1 + m2][k1])
+//   stage 3  role (k1, j1):     X[k1 + 7 j1 + 56 j2] = DFT8_{m2}(B[k1][m2][j1] * w64^{m2 j1})
+// so role g < 56 ends holding X[k1 + 7 j1 + 56 j2], j2 = 0..7, (k1, j1) = (g/8, g%8).
+// The inverse runs the same stages transposed (permuted in, natural out) with
+// conjugate twiddles, so a forward -> pointwise -> inverse chain never
+// reorders.  The 64 roles of a transform are folded onto the 32 lanes of one
+// warp: lane l plays roles r = l and r = l + 32 ("halves" h = 0, 1).  Radix-8
+// stages have 56 groups; half 1 is active on lanes < 24.
 //   forward:  in  a[h][n1] = x[64 n1 + l + 32 h]          (all lanes, both halves)
 //             out b[h][j2] = X[k1 + 7 j1 + 56 j2], g = l + 32 h < 56, (k1, j1) = (g >> 3, g & 7)
 //   inverse (transposed stages, conjugate twiddles): the reverse mapping.
