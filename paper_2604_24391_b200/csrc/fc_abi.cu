@@ -220,7 +220,13 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
     fc<<<dim3(kp.NRG, B), blk, pl->smemC, st>>>(kp);
     if (rec) rec->mark(st, 2);
   }
-  k_select<<<B, FC_SEL_THREADS, pl->smemD, st>>>(kp, cfg, out);
+  // small batches leave SMs idle during the per-stream selection: give each
+  // stream more threads there (FC_SEL_NT overrides)
+  static const int nt_env = env_int("FC_SEL_NT", 0, 0, 1024);
+  const int nt = nt_env ? nt_env : (B <= 128 ? 512 : FC_SEL_THREADS);
+  if (nt >= 1024) k_select<1024><<<B, 1024, pl->smemD, st>>>(kp, cfg, out);
+  else if (nt >= 512) k_select<512><<<B, 512, pl->smemD, st>>>(kp, cfg, out);
+  else k_select<FC_SEL_THREADS><<<B, FC_SEL_THREADS, pl->smemD, st>>>(kp, cfg, out);
   if (rec) rec->mark(st, 3);
 }
 
@@ -373,7 +379,9 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
       if (rc == FC_OK) rc = set_smem(sel_cols(pl->kh), pl->smemB);
       if (rc == FC_OK) rc = set_smem(sel_rows_inv(pl->kw), pl->smemC);
     }
-    if (rc == FC_OK) rc = set_smem((void*)k_select, pl->smemD);
+    if (rc == FC_OK) rc = set_smem((void*)k_select<FC_SEL_THREADS>, pl->smemD);
+    if (rc == FC_OK) rc = set_smem((void*)k_select<512>, pl->smemD);
+    if (rc == FC_OK) rc = set_smem((void*)k_select<1024>, pl->smemD);
   }
   if (rc != FC_OK) {
     fc_plan_destroy(pl);

@@ -672,8 +672,8 @@ __device__ void bitonic_hybrid(double* ke, int* ki, int NP2) {
 
 // Decision for one stream (fusion.py:121-242 selection; 245-262 invariants
 // hold by construction).  Scalars in thread 0, per-token work spread.
-__global__ void __launch_bounds__(FC_SEL_THREADS) k_select(KParams kp, fc_config cfg,
-                                                           fc_select_out out) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_select_out out) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int b = blockIdx.x;
   const int N = kp.N;
