@@ -9,7 +9,7 @@ it, and only as the checker / the timed CPU baseline.  The product path
 
 Pinning: the restatement is checked against (a) golden decisions produced by
 running the reference itself in the build container
-(``tests/golden/make_golden.py`` -> ``tests/golden/*.npz``) and (b) the
+(``tests/golden/make_golden.py`` -> ``tests/golden/golden_*.json``) and (b) the
 known-answer values the reference's own tests hold (see
 ``tests/test_oracle_golden.py``).
 
