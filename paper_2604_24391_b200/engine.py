@@ -12,6 +12,7 @@ stream, so whole steps can be captured in a CUDA graph.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import torch
@@ -84,7 +85,6 @@ class FreqCacheEngine:
         self.cols = self.width // self.patch_size
         self.n_tokens = self.lib.fc_plan_tokens(plan)
         fast = (self.height, self.width, self.patch_size) == (448, 448, 14)
-        import os
         chunk = min(self.batch, max(1, int(os.environ.get("FC_CHUNK", "512"))))
         self.launches_per_select = (3 * -(-self.batch // chunk) + 1) if fast else 4
         sb = self.lib.fc_plan_state_bytes(plan)
