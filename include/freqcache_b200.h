@@ -136,7 +136,9 @@ int  fc_state_reset(const fc_plan* plan, void* state, int32_t first,
                     int32_t count, void* cuda_stream);
 
 /* One decision step for all B streams (frames: [B] frames in geometry's
- * format).  Cold streams only establish their spectrum (result.cold = 1). */
+ * format).  Cold streams only establish their spectrum (result.cold = 1).
+ * state and workspace must be 16-byte aligned, and so must frames at
+ * 448 x 448 / P 14 (bulk copies); FC_EINVAL otherwise. */
 int  fc_select(const fc_plan* plan, const fc_config* cfg, const void* frames,
                void* state, void* workspace, const fc_select_out* out,
                void* cuda_stream);

@@ -426,6 +426,10 @@ int fc_state_reset(const fc_plan* pl, void* state, int32_t first, int32_t count,
 int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
               const fc_select_out* out, void* stream) {
   if (!pl || !cfg || !frames || !state || !ws || !out) return FC_EINVAL;
+  // bulk (TMA) copies stage state and workspace (and the fast path's frames): 16-byte alignment
+  if (((pl->fast ? reinterpret_cast<uintptr_t>(frames) : 0) | reinterpret_cast<uintptr_t>(state) |
+       reinterpret_cast<uintptr_t>(ws)) & 15)
+    return FC_EINVAL;
   const int rc = check_cfg(cfg);
   if (rc != FC_OK) return rc;
   const KParams kp = bind(pl, state, ws, out->energy);
@@ -436,6 +440,9 @@ int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void*
 int fc_select_profile(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
                       const fc_select_out* out, float* kernel_ms, void* stream) {
   if (!pl || !cfg || !frames || !state || !ws || !out || !kernel_ms) return FC_EINVAL;
+  if (((pl->fast ? reinterpret_cast<uintptr_t>(frames) : 0) | reinterpret_cast<uintptr_t>(state) |
+       reinterpret_cast<uintptr_t>(ws)) & 15)
+    return FC_EINVAL;
   int rc = check_cfg(cfg);
   if (rc != FC_OK) return rc;
   const cudaStream_t st = as_stream(stream);
@@ -510,6 +517,7 @@ int fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t*
               const int64_t* cache_ages, const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* out,
               int64_t* out_ages, void* stream) {
   if (batch < 1 || n_tokens < 1 || row_bytes < 1 || !src_map || !fresh || !out || !out_ages) return FC_EINVAL;
+  if ((int64_t)batch * n_tokens > INT32_MAX) return FC_EINVAL;
   if (fresh_layout != FC_FRESH_DENSE && fresh_layout != FC_FRESH_COMPACT) return FC_EINVAL;
   if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
   if (fresh_rows < 1) return FC_EINVAL;
@@ -522,6 +530,7 @@ int fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes, const i
                      const int64_t* fresh_offsets, void* out, int64_t* out_ages, void* stream) {
   if (batch < 1 || n_tokens < 1 || row_bytes < 1 || !src_map || !fresh || !fresh_offsets || !out || !out_ages)
     return FC_EINVAL;
+  if ((int64_t)batch * n_tokens > INT32_MAX) return FC_EINVAL;
   return splice_impl(batch, n_tokens, row_bytes, src_map, cache, cache_ages, fresh, 1, 0, fresh_offsets, out,
                      out_ages, as_stream(stream));
 }
@@ -540,7 +549,9 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
         reinterpret_cast<uintptr_t>(fresh)) & 15) != 0)
     return FC_EINVAL;
   if (fresh_layout != FC_FRESH_DENSE && fresh_layout != FC_FRESH_COMPACT) return FC_EINVAL;
+  if ((int64_t)batch * n_tokens > INT32_MAX || row_bytes > INT32_MAX) return FC_EINVAL;
   if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
+  if (fresh_rows < 1) return FC_EINVAL;
   const cudaStream_t st = as_stream(stream);
   int32_t* rows = reinterpret_cast<int32_t*>(scratch);
   int32_t* counts = rows + (size_t)batch * n_tokens;

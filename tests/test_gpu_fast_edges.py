@@ -136,3 +136,20 @@ def test_generic_path_envelope(cuda, h, w, p):
             o = O.decide(fr[t - 1, s], fr[t, s], oc, step=t)
             compare(d, o, oc, energies=en[s], rep=rep)
     assert rep.ok, rep.errors
+
+
+def test_fast_path_refuses_misaligned_frames(cuda):
+    # K_A stages frames with bulk copies: a frames pointer off 16 bytes is
+    # refused up front (FC_EINVAL -> ValueError) instead of faulting
+    import torch
+    import paper_2604_24391_b200 as fc
+    eng = fc.FreqCacheEngine(2, H, H, P, fmt="rgb")
+    n = 2 * H * H * 3
+    buf = torch.zeros(n + 1, dtype=torch.float32, device="cuda")
+    frames = buf[1:].view(2, H, H, 3)
+    assert frames.is_contiguous() and frames.data_ptr() % 16 == 4
+    with pytest.raises(ValueError):
+        eng.select(frames, fc.CacheConfig(patch_size=P))
+    out = eng.select(buf[:n].view(2, H, H, 3), fc.CacheConfig(patch_size=P))   # aligned: fine
+    torch.cuda.synchronize()
+    assert (out.host_results()["cold"] == 1).all()

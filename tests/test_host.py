@@ -50,6 +50,21 @@ def test_plan_rejects_bad_geometry_without_device(lib):
     assert rc == _native.FC_EUNSUPPORTED
 
 
+def test_splice_rejects_bad_arguments_without_device(lib):
+    # argument checks return before any device call (fc_abi.cu fc_splice / fc_splice_inplace)
+    from paper_2604_24391_b200 import _native
+    p = ctypes.c_void_p(4096)   # never dereferenced: every call below is refused first
+    big = 1 << 16
+    assert lib.fc_splice(big, big, 32, p, p, p, p, 0, 0, p, p, None) == _native.FC_EINVAL
+    assert lib.fc_splice(1, 4, 32, p, p, p, p, 7, 0, p, p, None) == _native.FC_EINVAL
+    assert lib.fc_splice(1, 4, 32, p, p, p, p, 1, 0, p, p, None) == _native.FC_EINVAL   # compact, no rows
+    assert lib.fc_splice_inplace(big, big, 32, p, p, p, p, p, p, p, p, 0, 0, p, None) == _native.FC_EINVAL
+    assert lib.fc_splice_inplace(1, 4, 24, p, p, p, p, p, p, p, p, 0, 0, p, None) == _native.FC_EINVAL
+    assert lib.fc_splice_inplace(1, 4, 32, p, p, p, p, p, p, p, p, 1, 0, p, None) == _native.FC_EINVAL
+    assert lib.fc_splice_inplace(1, 4, 32, p, ctypes.c_void_p(4100), p, p, p, p, p, p, 0, 0, p,
+                                 None) == _native.FC_EINVAL   # misaligned cache
+
+
 def test_product_path_fails_loudly_without_gpu():
     import torch
     if torch.cuda.is_available():
