@@ -72,7 +72,9 @@ def main(tag):
              f"(select {bench['roofline_step']['select_bytes']} B + splice {bench['roofline_step']['splice_bytes']} B per frame); "
              f"clocks {bench['clocks']}.",
              f"e2e (pinned host frames, H2D {bench['e2e']['h2d_bytes_per_step'] / 1e9:.2f} GB/step): "
-             f"{bench['e2e']['value']:.0f} frames/s.  CPU baseline ({bench['cpu_baseline']['kind']}, "
+             f"{bench['e2e']['value']:.0f} frames/s"
+             + (f" (frames as P6 uint8 payloads: {bench['e2e_u8']['value']:.0f} frames/s)" if "e2e_u8" in bench else "")
+             + f".  CPU baseline ({bench['cpu_baseline']['kind']}, "
              f"{bench['cpu_baseline']['cores']} cores): {bench['cpu_baseline']['value']:.0f} frames/s.", "",
              "## Launch list (ncu `gpu__time_duration.sum`, serialised, cold cache)", "",
              "| kernel | launches | mean us | share |", "|---|---|---|---|"]
