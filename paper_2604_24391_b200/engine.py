@@ -270,6 +270,11 @@ def splice_packed(src_map, cache, cache_ages, fresh_values, fresh_offsets, out, 
         raise ValueError("fresh_values must be [total, D] with out's dtype")
     if fresh_offsets.dtype != torch.int64 or fresh_offsets.numel() < B:
         raise ValueError("fresh_offsets must be int64 [B]")
+    for t in (src_map, fresh_values, fresh_offsets, out, out_ages) + ((cache, cache_ages) if cache is not None else ()):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("splice operands must be contiguous CUDA tensors")
+    if cache is not None and (cache.dtype != out.dtype or cache.shape != out.shape):
+        raise ValueError("cache and out must share dtype and shape")
     rc = lib.fc_splice_packed(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(cache), _ptr(cache_ages),
                               _ptr(fresh_values), _ptr(fresh_offsets), _ptr(out), _ptr(out_ages),
                               _stream(out.device))
