@@ -822,11 +822,17 @@ __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_sel
   }
   __syncthreads();
 
-  // Module II statistics (edge_refresh.py:62-73): population mean / std
+  // Module II statistics (edge_refresh.py:62-73): population mean / std.
+  // Summation order fixed at FC_SEL_THREADS strided partials whatever the
+  // block size (the extra warps add exact zeros to the trees), so a stream's
+  // statistics do not depend on the batch size that picked the block size.
+  static_assert(NT % FC_SEL_THREADS == 0, "block size must be a multiple of the reduction width");
+  const bool red_lane = threadIdx.x < FC_SEL_THREADS;
   double s1 = 0.0;
   // shifted by E[0]: an all-equal energy map keeps an exact mean and std 0
   const double e0 = E[0];
-  for (int p = threadIdx.x; p < N; p += blockDim.x) s1 += E[p] - e0;
+  if (red_lane)
+    for (int p = threadIdx.x; p < N; p += FC_SEL_THREADS) s1 += E[p] - e0;
   {
     double v[1] = {s1};
     block_sum_d<1>(v, red);
@@ -835,7 +841,8 @@ __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_sel
   __syncthreads();
   const double mu = red[63];
   double s2 = 0.0;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) { const double d = E[p] - mu; s2 = fma(d, d, s2); }
+  if (red_lane)
+    for (int p = threadIdx.x; p < N; p += FC_SEL_THREADS) { const double d = E[p] - mu; s2 = fma(d, d, s2); }
   {
     double v[1] = {s2};
     block_sum_d<1>(v, red);
