@@ -106,3 +106,43 @@ def test_config5_full_size_properties(cuda):
             d = decision_from_device(res[s], ri[s], rc[s], out.refresh_mask[s].cpu().numpy(), step=t)
             compare(d, O.decide(f0[k], f1[k], oc, step=t), oc, energies=out.energy[s].cpu().numpy(), rep=rep)
     assert rep.ok, rep.errors
+
+
+def test_config5_full_size_shifted_inplace_splice(cuda):
+    """The in-place splice copier at the bench size (512 streams x 1024 x
+    1152 bf16) with every kind of stream in one batch — zero displacement
+    (updated in place), shifted by up to one patch (ping-pong to the other
+    buffer), flushed — over several steps, against the gather each step's
+    map defines (tokens bit for bit, ages)."""
+    import torch
+    import paper_2604_24391_b200 as fc
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(11)
+    cache = torch.empty((2, S, N, D), dtype=torch.bfloat16, device=dev)
+    cache[0].normal_(generator=g)
+    ages = torch.zeros((2, S, N), dtype=torch.int64, device=dev)
+    ages[0] = torch.randint(0, 9, (S, N), generator=g, device=dev)
+    state = fc.SpliceState(cache, ages)
+    cols = H // P
+    ii = (torch.arange(N, device=dev) // cols)[None]
+    jj = (torch.arange(N, device=dev) % cols)[None]
+    for stepi in range(4):
+        kind = torch.randint(0, 4, (S,), generator=g, device=dev)            # 0, 1: zero shift; 2: shifted; 3: flush
+        dip = torch.where(kind == 2, torch.randint(-1, 2, (S,), generator=g, device=dev), 0)
+        djp = torch.where(kind == 2, torch.randint(-1, 2, (S,), generator=g, device=dev), 0)
+        si, sj = ii - dip[:, None], jj - djp[:, None]
+        aligned = (si >= 0) & (si < cols) & (sj >= 0) & (sj < cols)
+        reuse = aligned & (torch.rand((S, N), generator=g, device=dev) < 0.45) & (kind != 3)[:, None]
+        rank = torch.cumsum((~reuse).to(torch.int32), dim=1) - 1
+        src = torch.where(reuse, si * cols + sj, -(rank + 1)).to(torch.int32).contiguous()
+        fresh = torch.empty((S, N, D), dtype=torch.bfloat16, device=dev).normal_(generator=g)
+        before_tok, before_age = state.current()
+        state.step(src, fresh)
+        after_tok, after_age = state.current()
+        s64 = src.long().clamp(min=0)
+        exp_tok = torch.where(reuse[..., None], torch.gather(before_tok, 1, s64[..., None].expand(-1, -1, D)), fresh)
+        exp_age = torch.where(reuse, torch.gather(before_age, 1, s64) + 1, torch.zeros_like(before_age))
+        assert torch.equal(after_tok.view(torch.int16), exp_tok.view(torch.int16)), stepi
+        assert torch.equal(after_age, exp_age), stepi
+        del before_tok, exp_tok, after_tok
