@@ -31,7 +31,7 @@ constexpr int kThreadsA448 = 224;
 // both, and the per-warp FFT scratch 7 x 504 after them
 constexpr int kZinBytes = 7 * 448 * 8;
 constexpr int kPartBytes = (4 * 480 + 288) * 8;
-static_assert(448 * 9 * 8 <= kZinBytes + kPartBytes, "zout must not reach the FFT scratch");
+static_assert((9 * 447 + 3 * (447 / 7) + 7) * 8 <= kZinBytes + kPartBytes, "zout must not reach the FFT scratch");
 static_assert(kZinBytes + kPartBytes + 7 * 504 * 8 <= kPxBytes448, "K_A shared memory");
 
 // Gray values of two horizontally adjacent pixels i, i + 1 (i even).
@@ -175,8 +175,9 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
   w448::TwLazy tw;
   tw.load(kp.tw448, kp.tw64, lane);
   w448::fwd<false>(a, bv, S, lane, tw);  // private scratch
-  // zout[k][9]: bin k of pair g at k * 9 + g, over zin and part (every warp
-  // has loaded its zin row and phase 2 is done after this barrier)
+  // zout: bin k of pair g at 9 k + g + 3 (k / 7), over zin and part (every
+  // warp has loaded its zin row and phase 2 is done after this barrier); the
+  // 3-slot skip every 7 bins makes the stores below bank-conflict free
   __syncthreads();
   float2* zout = zin;
 #pragma unroll
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
     if (h == 0 || lane < 24) {
       const int k1 = (lane >> 3) + 4 * h, j1 = lane & 7;
 #pragma unroll
-      for (int j2 = 0; j2 < 8; ++j2) zout[(k1 + 7 * j1 + 56 * j2) * 9 + g] = bv[h][j2];
+      for (int j2 = 0; j2 < 8; ++j2) zout[(k1 + 7 * j1 + 56 * j2) * 9 + g + 3 * (j1 + 8 * j2)] = bv[h][j2];
     }
   }
   __syncthreads();
@@ -196,15 +197,16 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
   {
     const int gg = t % 7, q0 = t / 7;
     float4* dst = reinterpret_cast<float4*>(kp.T + (size_t)bl * 224 * 448 + s * 14 + 2 * gg);
+    auto zo = [](int k) { return 9 * k + 3 * (k / 7); };
     if (q0 == 0) {
-      const float2 z0 = zout[gg], zn = zout[224 * 9 + gg];
+      const float2 z0 = zout[gg], zn = zout[zo(224) + gg];
       dst[0] = make_float4(z0.x, zn.x, z0.y, zn.y);
     }
 #pragma unroll
     for (int i = 0; i < 7; ++i) {
       const int q = q0 + 32 * i;
       if (q == 0) continue;
-      const float2 za = zout[q * 9 + gg], zm = zout[(448 - q) * 9 + gg];
+      const float2 za = zout[zo(q) + gg], zm = zout[zo(448 - q) + gg];
       dst[(size_t)q * 224] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y),
                                          0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
     }
