@@ -155,7 +155,8 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []          # (host time, csv line)
+        self.window = None       # host-time bounds of the timed region
 
     def __enter__(self):
         try:
@@ -165,13 +166,26 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a moment before its first sample: wait for it
+            # so the timed region (~0.1 s at the default size) is covered
+            t_end = time.monotonic() + 5.0
+            while not self.lines and time.monotonic() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def start(self):
+        self.window = [time.monotonic(), None]
+
+    def stop(self):
+        # a sample is read shortly after it is taken: allow about one period
+        time.sleep(0.03)
+        self.window[1] = time.monotonic()
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -184,7 +198,10 @@ class ClockSampler:
     def summary(self):
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo, hi = self.window if self.window and self.window[1] else (float("-inf"), float("inf"))
+        for ts, ln in self.lines:
+            if not (lo <= ts <= hi):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -323,8 +340,12 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # clock sampling starts before the warm-up, so the GPU does not idle while
+    # nvidia-smi starts; only samples inside the timed region are kept
+    clocks = ClockSampler(local).__enter__()
     # ---- warm-up (step 0 establishes every stream's spectrum)
-    for t in range(a.warmup):
+    w0 = a.warmup
+    for t in range(w0):
         pipe_step(t)
     drain()
     barrier()
@@ -333,14 +354,18 @@ def run_ours(a):
     stream = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches[0] = 0
-    with ClockSampler(local) as clocks:
+    try:
         barrier()
+        clocks.start()
         ev0.record(stream)
-        for t in range(a.warmup, a.warmup + a.steps):
+        for t in range(w0, w0 + a.steps):
             pipe_step(t)
         drain()
         ev1.record(stream)
         barrier()
+        clocks.stop()
+    finally:
+        clocks.__exit__(None, None, None)
     gpu_launches = launches[0]
     ms = ev0.elapsed_time(ev1)
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -352,7 +377,7 @@ def run_ours(a):
 
     # decision statistics of the last timed step over all ranks (the only
     # other collective: a few counters, NCCL all-reduce over NVLink)
-    res = outs[(a.warmup + a.steps - 1) & 1].host_results()
+    res = outs[(w0 + a.steps - 1) & 1].host_results()
     cnt = gather_counters(step_counters(res), device=dev)
     reuse_ratio = cnt["reused_tokens"] / cnt["tokens"]
     flush_rate = cnt["flushes"] / cnt["frames"]
@@ -361,7 +386,7 @@ def run_ours(a):
     kp_steps = min(a.steps, 16)
     names = ["rows_fwd", "cols", "rows_inv", "select", "splice"]
     kms = [0.0] * 5
-    t0 = a.warmup + a.steps
+    t0 = w0 + a.steps
     for t in range(t0, t0 + kp_steps):
         one_step(t, kernel_ms=kms)
     kms = [v / kp_steps for v in kms]
