@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
                                                                 int b0, int do_fft) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[7];
+  __shared__ int sh_bad;
   constexpr int bpp = FMT == FC_FMT_RGB_F32 ? 12 : FMT == FC_FMT_GRAY_F32 ? 4 : FMT == FC_FMT_GRAY_U8 ? 1
                     : FMT == FC_FMT_RGB_U8 ? 3 : 8;
   constexpr uint32_t pair_bytes = 2 * 448 * bpp;
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
   // ---- phase 0: stage the stripe with the TMA engine, one copy per row pair
   const size_t row0 = ((size_t)b * 448 + (size_t)s * 14) * 448;
   if (t == 0) {
+    sh_bad = 0;
 #pragma unroll
     for (int g = 0; g < 7; ++g) tma::bar_init(&bar[g], 1);
     const char* src = reinterpret_cast<const char*>(frames) + row0 * bpp;
@@ -117,8 +119,9 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
   }
   const int anyvary = __syncthreads_or(vary);  // also: every pixel has been read
   // a NaN / Inf pixel makes its column's sum of squares non-finite (the
-  // squares of finite fp32-derived values cannot overflow fp64)
-  const int anybad = __syncthreads_or(!isfinite(s2[0]) || !isfinite(s2[1]));
+  // squares of finite fp32-derived values cannot overflow fp64); the flag is
+  // read after the next barrier
+  if (!isfinite(s2[0]) || !isfinite(s2[1])) sh_bad = 1;
   // fp32 gray as packed row pairs (2g, 2g+1), over the consumed stripe
 #pragma unroll
   for (int g = 0; g < 7; ++g)
@@ -135,13 +138,13 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
     pc[2 * 480] = tu2[c];
     pc[3 * 480] = s2[c];
   }
+  __syncthreads();
   if (t == 0) {
     StripeStat st;
-    st.ref = ref; st.unused = 0.0; st.nonfinite = anybad; st.varying = anyvary;
+    st.ref = ref; st.unused = 0.0; st.nonfinite = sh_bad; st.varying = anyvary;
     st.pad[0] = st.pad[1] = 0;
     kp.stripes[(size_t)b * 32 + s] = st;
   }
-  __syncthreads();
   // ---- phase 2: low-frequency corner per patch (fp64); (u, v) x patch
   for (int i = t; i < 288; i += kThreadsA448) {
     const int uv = i >> 5, pp = i & 31, u = uv / 3, v = uv - (uv / 3) * 3;
