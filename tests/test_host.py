@@ -50,6 +50,36 @@ def test_plan_rejects_bad_geometry_without_device(lib):
     assert rc == _native.FC_EUNSUPPORTED
 
 
+def test_plan_geometry_validation_property(lib):
+    """fc_plan_create over random geometries: every invalid one (frame.py:31-37
+    rules, bad format) is refused with FC_EINVAL, sizes beyond the kernel
+    envelope with FC_EUNSUPPORTED, before any device call; valid ones are never
+    refused as invalid (without a device they stop at FC_ECUDA)."""
+    from hypothesis import given, settings, strategies as st
+    from paper_2604_24391_b200 import _native
+
+    @settings(max_examples=300, deadline=None, derandomize=True)
+    @given(st.integers(-2, 6), st.integers(-3, 2000), st.integers(-3, 2000), st.integers(-1, 70),
+           st.integers(-2, 7))
+    def prop(batch, h, w, p, fmt):
+        plan = ctypes.c_void_p()
+        rc = lib.fc_plan_create(ctypes.byref(_native.Geometry(batch, h, w, p, fmt)), ctypes.byref(plan))
+        invalid = (batch < 1 or h < 1 or w < 1 or p < 2 or h % p or w % p
+                   or not (_native.FC_FMT_RGB_F32 <= fmt <= _native.FC_FMT_RGB_U8))
+        if invalid:
+            assert rc == _native.FC_EINVAL
+        elif h > 1536 or w > 1536:
+            assert rc == _native.FC_EUNSUPPORTED
+        else:
+            assert rc in (_native.FC_OK, _native.FC_EUNSUPPORTED, _native.FC_ECUDA)
+        if rc == _native.FC_OK:
+            lib.fc_plan_destroy(plan)
+        else:
+            assert not plan.value
+
+    prop()
+
+
 def test_splice_rejects_bad_arguments_without_device(lib):
     # argument checks return before any device call (fc_abi.cu fc_splice / fc_splice_inplace)
     from paper_2604_24391_b200 import _native
