@@ -9,6 +9,8 @@
 //           stream each) stay L2-resident between the three FFT kernels;
 //   generic any other geometry inside the envelope: shared-memory Stockham
 //           FFTs with runtime radix plans (fc_fft.cuh / fc_kernels.cuh).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -47,6 +49,7 @@ struct fc_plan {
   cudaEvent_t join[kMaxLanes] = {};
   size_t lane_stride = 0;              // workspace bytes per lane (T1 + T2)
   void* fnB = nullptr;                 // K_B / K_C variants (occupancy x twiddle mode)
+  bool t2_tma = false;                 // K_B stores T2 with a TMA tensor store
   void* fnC = nullptr;
   float2* d_twW = nullptr;
   float2* d_twH = nullptr;
@@ -171,6 +174,34 @@ struct Recorder {
   }
 };
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// T2 of one lane as a 2-D tensor: rows = row pairs of `chunk` streams, each
+// 224 columns x 16 bytes (as u32); box = 4 columns x 224 row pairs with the
+// 64-byte swizzle K_B's tile uses.
+bool encode_t2_map(CUtensorMap* map, void* t2, int chunk) {
+  const PFN_cuTensorMapEncodeTiled enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {224 * 4, (cuuint64_t)chunk * 224};
+  const cuuint64_t strides[1] = {224 * 16};
+  const cuuint32_t box[2] = {kWarpsB * 4, 224};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, t2, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, const KParams& kp,
                    const fc_select_out& out, cudaStream_t st, Recorder* rec) {
   const int B = pl->g.batch;
@@ -195,8 +226,11 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
       fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1);
       if (rec) rec->mark(st, 0);
-      auto fb = (void (*)(KParams, int))pl->fnB;
-      fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0);
+      CUtensorMap tm;
+      std::memset(&tm, 0, sizeof(tm));
+      if (pl->t2_tma) encode_t2_map(&tm, kl.T2, pl->chunk);   // checked at plan creation
+      auto fb = (void (*)(KParams, int, CUtensorMap))pl->fnB;
+      fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm);
       if (rec) rec->mark(st, 1);
       auto fc = (void (*)(KParams, int))pl->fnC;
       fc<<<dim3(kNRG448, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
@@ -368,8 +402,17 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
       // occupancy variants: FC_OCC_B / FC_OCC_C = target CTAs per SM (register
       // cap); twiddles are read at use (lazy) when the cap is tight
       const int ob = env_int("FC_OCC_B", 6, 4, 8), oc = env_int("FC_OCC_C", 7, 4, 10);
-      pl->fnB = ob >= 6 ? (void*)k448_cols<6, true> : ob == 5 ? (void*)k448_cols<5, false>
-              : (void*)k448_cols<4, false>;
+      // T2 by TMA tensor store (FC_T2_TMA=0: copy loop) when the driver offers
+      // the tensor-map encoder
+      pl->t2_tma = env_int("FC_T2_TMA", 1, 0, 1) && tensor_map_encoder() != nullptr;
+      if (pl->t2_tma) {
+        CUtensorMap probe;   // parameters check only (no memory access)
+        pl->t2_tma = encode_t2_map(&probe, reinterpret_cast<void*>(256), pl->chunk);
+      }
+      pl->fnB = pl->t2_tma ? (ob >= 6 ? (void*)k448_cols<6, true, true> : ob == 5 ? (void*)k448_cols<5, false, true>
+                                                                            : (void*)k448_cols<4, false, true>)
+                           : (ob >= 6 ? (void*)k448_cols<6, true, false> : ob == 5 ? (void*)k448_cols<5, false, false>
+                                                                             : (void*)k448_cols<4, false, false>);
       pl->fnC = oc >= 10 ? (void*)k448_rows_inv<10, true> : oc >= 8 ? (void*)k448_rows_inv<8, true>
               : oc == 7 ? (void*)k448_rows_inv<7, true> : (void*)k448_rows_inv<6, false>;
       if (rc == FC_OK) rc = set_smem(pl->fnB, pl->smemB);

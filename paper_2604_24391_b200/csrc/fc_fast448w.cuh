@@ -30,7 +30,7 @@ constexpr int kNRG448 = 224 / kWarpsC;     // K_C CTAs per stream = peak partial
 constexpr int kStCol = 2 * 4 * 32;         // float4 per state column
 constexpr int kSlotB = 512;                // float2: T1 column (448), then FFT scratch (504)
 constexpr int kSmemB448 = kWarpsB * (kSlotB * 8 + kStCol * 16);
-static_assert(kWarpsB == 4 && 224 * 4 * 16 <= kWarpsB * kStCol * 16, "T2 tile must fit the prev blocks");
+static_assert(kWarpsB == 4 && 224 * 4 * 16 + 1023 <= kWarpsB * kStCol * 16, "T2 tile (aligned) must fit the prev blocks");
 constexpr int kSmemC448 = kWarpsC * w448::XS * 8;
 
 template <bool LAZY>
@@ -50,8 +50,11 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 // normalised cross-power (migration.py:128-131) and the inverse column FFT
 // into T2.  Column 0 holds the packed DC / Nyquist columns (real along rows),
 // unpacked with bins k and 448 - k of the same column.
-template <int MINB, bool LAZY>
-__global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int b0) {
+// TMST: T2 leaves through one TMA tensor store per CTA (the tile's swizzle is
+// the tensor map's 64-byte swizzle) instead of a copy loop over the threads.
+template <int MINB, bool LAZY, bool TMST>
+__global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int b0,
+                                                               const __grid_constant__ CUtensorMap tmT2) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[kWarpsB][2];
   __shared__ double red[kWarpsB][4];
@@ -182,7 +185,10 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
   // the unit of column w in pair p sits at p * 4 + (w ^ ((p >> 1) & 3)), so
   // the writes below and the reads of the copy-out are conflict free
   __syncthreads();
-  float2* tile = reinterpret_cast<float2*>(smem + kWarpsB * kSlotB * 8);
+  // 1024-byte aligned inside the prev blocks (16 KB, the tile is 14 KB), so
+  // the swizzle below is the hardware's 64-byte pattern on absolute addresses
+  float2* tile = reinterpret_cast<float2*>(
+      (reinterpret_cast<uintptr_t>(smem + kWarpsB * kSlotB * 8) + 1023) & ~static_cast<uintptr_t>(1023));
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -196,12 +202,22 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
     for (int w = 0; w < kWarpsB; ++w) acc4 += red[w][threadIdx.x];
     kp.stats[((size_t)b * kNCB448 + blockIdx.x) * 4 + threadIdx.x] = acc4;
   }
-  __syncthreads();
-  const float4* t4 = reinterpret_cast<const float4*>(tile);
-  float4* T2 = reinterpret_cast<float4*>(kp.T2) + (size_t)bl * 224 * 224 + blockIdx.x * kWarpsB;
-  for (int u = threadIdx.x; u < 224 * 4; u += 32 * kWarpsB) {
-    const int pr = u >> 2, col = (u & 3) ^ ((pr >> 1) & 3);
-    T2[(size_t)pr * 224 + col] = t4[u];
+  if constexpr (TMST) {
+    tma::fence_async_shared();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // box = 4 columns (64 bytes) x 224 row pairs of this stream's T2 block
+      tma::tensor_store_2d(&tmT2, tile, blockIdx.x * kWarpsB * 4, bl * 224);
+      tma::bulk_wait_read0();  // the tile must stay until the engine has read it
+    }
+  } else {
+    __syncthreads();
+    const float4* t4 = reinterpret_cast<const float4*>(tile);
+    float4* T2 = reinterpret_cast<float4*>(kp.T2) + (size_t)bl * 224 * 224 + blockIdx.x * kWarpsB;
+    for (int u = threadIdx.x; u < 224 * 4; u += 32 * kWarpsB) {
+      const int pr = u >> 2, col = (u & 3) ^ ((pr >> 1) & 3);
+      T2[(size_t)pr * 224 + col] = t4[u];
+    }
   }
 }
 

@@ -2,6 +2,7 @@
 // mbarrier completion, for staging contiguous tiles: frame stripes, spectrum
 // column blocks and per-stream state blocks.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -40,6 +41,19 @@ __device__ __forceinline__ void load_tile(void* dst, const void* src, uint32_t b
     const uint32_t n = bytes - off < piece ? bytes - off : piece;
     bulk_g2s(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, n, bar);
   }
+}
+
+// Make this thread's generic-proxy shared-memory writes visible to the async
+// proxy (bulk / tensor copies issued after a following barrier).
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 2-D tensor store (TMA) of one box from shared memory at tensor coordinates
+// (x inner, y outer), as one bulk group.
+__device__ __forceinline__ void tensor_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
 // Bulk shared->global copy (one bulk group per call) and its group waits.
