@@ -50,6 +50,7 @@ struct fc_plan {
   size_t lane_stride = 0;              // workspace bytes per lane (T1 + T2)
   void* fnB = nullptr;                 // K_B / K_C variants (occupancy x twiddle mode)
   bool t2_tma = false;                 // K_B stores T2 with a TMA tensor store
+  bool t1_tma = false;                 // K_A stores T1 with a TMA tensor store
   void* fnC = nullptr;
   float2* d_twW = nullptr;
   float2* d_twH = nullptr;
@@ -108,13 +109,16 @@ void* sel_rows_fwd(int k) { return k == 448 ? ptr_rows_fwd<448>() : k == 224 ? p
 void* sel_cols(int k) { return k == 448 ? ptr_cols<448>() : k == 224 ? ptr_cols<224>() : ptr_cols<0>(); }
 void* sel_rows_inv(int k) { return k == 448 ? ptr_rows_inv<448>() : k == 224 ? ptr_rows_inv<224>() : ptr_rows_inv<0>(); }
 
-void* sel_fast_rows_fwd(int fmt) {
-  return fmt == FC_FMT_RGB_F32 ? (void*)k448_rows_fwd<FC_FMT_RGB_F32>
-       : fmt == FC_FMT_GRAY_F32 ? (void*)k448_rows_fwd<FC_FMT_GRAY_F32>
-       : fmt == FC_FMT_GRAY_U8 ? (void*)k448_rows_fwd<FC_FMT_GRAY_U8>
-       : fmt == FC_FMT_RGB_U8 ? (void*)k448_rows_fwd<FC_FMT_RGB_U8>
-                                : (void*)k448_rows_fwd<FC_FMT_GRAY_F64>;
+template <bool TM>
+void* sel_fast_rows_fwd_t(int fmt) {
+  return fmt == FC_FMT_RGB_F32 ? (void*)k448_rows_fwd<FC_FMT_RGB_F32, TM>
+       : fmt == FC_FMT_GRAY_F32 ? (void*)k448_rows_fwd<FC_FMT_GRAY_F32, TM>
+       : fmt == FC_FMT_GRAY_U8 ? (void*)k448_rows_fwd<FC_FMT_GRAY_U8, TM>
+       : fmt == FC_FMT_RGB_U8 ? (void*)k448_rows_fwd<FC_FMT_RGB_U8, TM>
+                                : (void*)k448_rows_fwd<FC_FMT_GRAY_F64, TM>;
 }
+void* sel_fast_rows_fwd(int fmt, bool tm) { return tm ? sel_fast_rows_fwd_t<true>(fmt) : sel_fast_rows_fwd_t<false>(fmt); }
+using FastRowsFwd = void (*)(KParams, Dct14, const void*, int, int, CUtensorMap);
 
 int set_smem(void* fn, size_t bytes) {
   if (bytes > 48 * 1024) {
@@ -202,6 +206,20 @@ bool encode_t2_map(CUtensorMap* map, void* t2, int chunk) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// T1 of one lane as a 2-D tensor: rows = packed columns q of `chunk` streams,
+// each 448 rows x 8 bytes (as u32); box = one stripe's 14 rows x 224 columns.
+bool encode_t1_map(CUtensorMap* map, void* t1, int chunk) {
+  const PFN_cuTensorMapEncodeTiled enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {448 * 2, (cuuint64_t)chunk * 224};
+  const cuuint64_t strides[1] = {448 * 8};
+  const cuuint32_t box[2] = {14 * 2, 224};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, t1, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, const KParams& kp,
                    const fc_select_out& out, cudaStream_t st, Recorder* rec) {
   const int B = pl->g.batch;
@@ -210,7 +228,7 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
     // (each lane owns its T1/T2 slice) so one chunk's tail overlaps the next
     // chunk's head; the caller stream forks to and joins from the lanes.
     // Profiling runs the chunks serially on the caller stream.
-    auto fa = (void (*)(KParams, Dct14, const void*, int, int))sel_fast_rows_fwd(pl->g.format);
+    auto fa = (FastRowsFwd)sel_fast_rows_fwd(pl->g.format, pl->t1_tma);
     const int nl = rec ? 1 : pl->lanes;
     if (!rec) {
       cudaEventRecord(pl->fork, st);
@@ -224,7 +242,10 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
       KParams kl = kp;
       kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride);
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
-      fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1);
+      CUtensorMap tm1;
+      std::memset(&tm1, 0, sizeof(tm1));
+      if (pl->t1_tma) encode_t1_map(&tm1, kl.T, pl->chunk);   // checked at plan creation
+      fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1, tm1);
       if (rec) rec->mark(st, 0);
       CUtensorMap tm;
       std::memset(&tm, 0, sizeof(tm));
@@ -398,7 +419,13 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
   }
   if (rc == FC_OK) {
     if (pl->fast) {
-      rc = set_smem(sel_fast_rows_fwd(g.format), pl->smemA);
+      // T1 by TMA tensor store (FC_T1_TMA=0: per-thread stores)
+      pl->t1_tma = env_int("FC_T1_TMA", 1, 0, 1) && tensor_map_encoder() != nullptr;
+      if (pl->t1_tma) {
+        CUtensorMap probe;   // parameters check only (no memory access)
+        pl->t1_tma = encode_t1_map(&probe, reinterpret_cast<void*>(256), pl->chunk);
+      }
+      rc = set_smem(sel_fast_rows_fwd(g.format, pl->t1_tma), pl->smemA);
       // occupancy variants: FC_OCC_B / FC_OCC_C = target CTAs per SM (register
       // cap); twiddles are read at use (lazy) when the cap is tight
       const int ob = env_int("FC_OCC_B", 6, 4, 8), oc = env_int("FC_OCC_C", 7, 4, 10);
@@ -517,8 +544,10 @@ int fc_patch_energy(const fc_plan* pl, const void* frames, void* ws, double* ene
   const KParams kp = bind(pl, nullptr, ws, energy);
   const cudaStream_t st = as_stream(stream);
   if (pl->fast) {
-    auto fn = (void (*)(KParams, Dct14, const void*, int, int))sel_fast_rows_fwd(pl->g.format);
-    fn<<<dim3(32, pl->g.batch), kThreadsA448, pl->smemA, st>>>(kp, pl->dct14, frames, 0, 0);
+    auto fn = (FastRowsFwd)sel_fast_rows_fwd(pl->g.format, pl->t1_tma);
+    CUtensorMap none;   // energies only: no T1 store
+    std::memset(&none, 0, sizeof(none));
+    fn<<<dim3(32, pl->g.batch), kThreadsA448, pl->smemA, st>>>(kp, pl->dct14, frames, 0, 0, none);
   } else {
     auto fn = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
     fn<<<dim3(kp.rows, pl->g.batch), FC_THREADS, pl->smemA, st>>>(kp, frames, 0);

@@ -33,6 +33,7 @@ constexpr int kZinBytes = 7 * 448 * 8;
 constexpr int kPartBytes = (4 * 480 + 288) * 8;
 static_assert((9 * 447 + 3 * (447 / 7) + 7) * 8 <= kZinBytes + kPartBytes, "zout must not reach the FFT scratch");
 static_assert(kZinBytes + kPartBytes + 7 * 504 * 8 <= kPxBytes448, "K_A shared memory");
+static_assert(224 * 112 + 127 <= 7 * 504 * 8, "T1 tile (aligned) must fit the FFT scratch");
 
 // Gray values of two horizontally adjacent pixels i, i + 1 (i even).
 template <int FMT>
@@ -60,9 +61,12 @@ __device__ __forceinline__ void smem_luma2(const unsigned char* px, int i, doubl
   }
 }
 
-template <int FMT>
+// TMST: the stripe's T1 block (224 columns x 14 rows) is assembled in shared
+// memory and leaves through one TMA tensor store instead of per-thread stores.
+template <int FMT, bool TMST>
 __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct14 dc, const void* __restrict__ frames,
-                                                                int b0, int do_fft) {
+                                                                int b0, int do_fft,
+                                                                const __grid_constant__ CUtensorMap tmT1) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[7];
   __shared__ int sh_bad;
@@ -199,7 +203,13 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
   // keeps row pair gg = t % 7 and walks columns t / 7 + 32 i (224 = 7 * 32).
   {
     const int gg = t % 7, q0 = t / 7;
-    float4* dst = reinterpret_cast<float4*>(kp.T + (size_t)bl * 224 * 448 + s * 14 + 2 * gg);
+    // TMST: tile [224 columns][7 row pairs] float4 over the FFT scratch (free
+    // after the barrier above), 128-byte aligned; else straight to T1
+    float4* tile = reinterpret_cast<float4*>(
+        (reinterpret_cast<uintptr_t>(smem + kZinBytes + kPartBytes) + 127) & ~static_cast<uintptr_t>(127));
+    float4* dst = TMST ? tile + gg
+                       : reinterpret_cast<float4*>(kp.T + (size_t)bl * 224 * 448 + s * 14 + 2 * gg);
+    constexpr int qstride = TMST ? 7 : 224;   // float4 per column
     auto zo = [](int k) { return 9 * k + 3 * (k / 7); };
     if (q0 == 0) {
       const float2 z0 = zout[gg], zn = zout[zo(224) + gg];
@@ -210,8 +220,17 @@ __global__ void __launch_bounds__(kThreadsA448, 3) k448_rows_fwd(KParams kp, Dct
       const int q = q0 + 32 * i;
       if (q == 0) continue;
       const float2 za = zout[zo(q) + gg], zm = zout[zo(448 - q) + gg];
-      dst[(size_t)q * 224] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y),
-                                         0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
+      dst[(size_t)q * qstride] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y),
+                                             0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
+    }
+    if constexpr (TMST) {
+      tma::fence_async_shared();
+      __syncthreads();
+      if (t == 0) {
+        // box = 14 rows (x: 28 floats) x 224 columns of stream bl's T1
+        tma::tensor_store_2d(&tmT1, tile, s * 28, bl * 224);
+        tma::bulk_wait_read0();
+      }
     }
   }
 }
