@@ -220,10 +220,23 @@ bool encode_t1_map(CUtensorMap* map, void* t1, int chunk) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, const KParams& kp,
-                   const fc_select_out& out, cudaStream_t st, Recorder* rec) {
+// Returns FC_OK, or FC_ECUDA (nothing launched) when a tensor map cannot be
+// encoded for this call's workspace.
+int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, const KParams& kp,
+                  const fc_select_out& out, cudaStream_t st, Recorder* rec) {
   const int B = pl->g.batch;
   if (pl->fast) {
+    // tensor maps of every lane's T1 / T2 first, so a failure launches nothing
+    CUtensorMap tm1[kMaxLanes], tm2[kMaxLanes];
+    std::memset(tm1, 0, sizeof(tm1));
+    std::memset(tm2, 0, sizeof(tm2));
+    const int nmaps = rec ? 1 : pl->lanes;
+    for (int l = 0; l < nmaps; ++l) {
+      uint8_t* t1 = reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride;
+      uint8_t* t2 = reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride;
+      if (pl->t1_tma && !encode_t1_map(&tm1[l], t1, pl->chunk)) return FC_ECUDA;
+      if (pl->t2_tma && !encode_t2_map(&tm2[l], t2, pl->chunk)) return FC_ECUDA;
+    }
     // Chunks of `chunk` streams run A -> B -> C on `lanes` internal streams
     // (each lane owns its T1/T2 slice) so one chunk's tail overlaps the next
     // chunk's head; the caller stream forks to and joins from the lanes.
@@ -242,16 +255,10 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
       KParams kl = kp;
       kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride);
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
-      CUtensorMap tm1;
-      std::memset(&tm1, 0, sizeof(tm1));
-      if (pl->t1_tma) encode_t1_map(&tm1, kl.T, pl->chunk);   // checked at plan creation
-      fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1, tm1);
+      fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1, tm1[l]);
       if (rec) rec->mark(st, 0);
-      CUtensorMap tm;
-      std::memset(&tm, 0, sizeof(tm));
-      if (pl->t2_tma) encode_t2_map(&tm, kl.T2, pl->chunk);   // checked at plan creation
       auto fb = (void (*)(KParams, int, CUtensorMap))pl->fnB;
-      fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm);
+      fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm2[l]);
       if (rec) rec->mark(st, 1);
       auto fc = (void (*)(KParams, int))pl->fnC;
       fc<<<dim3(kNRG448, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
@@ -283,6 +290,7 @@ void launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, 
   else if (nt >= 512) k_select<512><<<B, 512, pl->smemD, st>>>(kp, cfg, out);
   else k_select<FC_SEL_THREADS><<<B, FC_SEL_THREADS, pl->smemD, st>>>(kp, cfg, out);
   if (rec) rec->mark(st, 3);
+  return FC_OK;
 }
 
 }  // namespace
@@ -503,7 +511,8 @@ int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void*
   const int rc = check_cfg(cfg);
   if (rc != FC_OK) return rc;
   const KParams kp = bind(pl, state, ws, out->energy);
-  launch_select(pl, *cfg, frames, kp, *out, as_stream(stream), nullptr);
+  const int lrc = launch_select(pl, *cfg, frames, kp, *out, as_stream(stream), nullptr);
+  if (lrc != FC_OK) return lrc;
   return launch_check();
 }
 
@@ -526,8 +535,8 @@ int fc_select_profile(const fc_plan* pl, const fc_config* cfg, const void* frame
   r.kind = kind.data();
   r.cap = cap;
   r.mark(st, -1);
-  launch_select(pl, *cfg, frames, kp, *out, st, &r);
-  rc = launch_check();
+  rc = launch_select(pl, *cfg, frames, kp, *out, st, &r);
+  if (rc == FC_OK) rc = launch_check();
   cudaStreamSynchronize(st);
   for (int k = 0; k < 4; ++k) kernel_ms[k] = 0.f;
   for (int i = 1; i < r.n; ++i) {
