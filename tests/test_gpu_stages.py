@@ -353,3 +353,33 @@ def test_inplace_splice_matches_oracle(cuda):
             assert np.array_equal(tok[b].view(torch.int16).cpu().numpy(), exp), (stepi, b)
             assert np.array_equal(age[b].cpu().numpy(), exp_age), (stepi, b)
             ref_tok[b], ref_age[b] = exp, exp_age
+
+
+def test_tensor_store_variants_bit_identical(cuda, monkeypatch):
+    """K_A / K_B write T1 / T2 with TMA tensor stores by default; the
+    per-thread store variants (FC_T1_TMA=0, FC_T2_TMA=0) compute the same
+    values, so every output must be bit-identical (checks the tensor maps'
+    layout and swizzle, including the multi-lane path)."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    S = 40
+    frames = torch_stream_frames(S, 3, 448, 448, seed=123, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    engines = []
+    for t1, t2, chunk, lanes in (("1", "1", "512", "1"), ("0", "0", "512", "1"), ("1", "0", "16", "2"),
+                                 ("0", "1", "16", "3")):
+        monkeypatch.setenv("FC_T1_TMA", t1)
+        monkeypatch.setenv("FC_T2_TMA", t2)
+        monkeypatch.setenv("FC_CHUNK", chunk)
+        monkeypatch.setenv("FC_LANES", lanes)
+        engines.append(fc.FreqCacheEngine(S, 448, 448, 14, fmt="rgb"))
+    for t in range(3):
+        outs = [e.select(frames[t], cfg, refresh_shift=1) for e in engines]
+        for o in outs[1:]:
+            assert torch.equal(o.results, outs[0].results)
+            assert torch.equal(o.reuse_idx, outs[0].reuse_idx)
+            assert torch.equal(o.src_map, outs[0].src_map)
+            assert torch.equal(o.energy, outs[0].energy)
+    for e in engines:
+        assert torch.equal(e.state, engines[0].state)   # previous-frame spectra, bit for bit
