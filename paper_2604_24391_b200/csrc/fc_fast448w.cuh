@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, 
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ PeakKey redk[kWarpsC];
   __shared__ float redv[kWarpsC];
+  __shared__ __align__(8) uint64_t barc[kWarpsC];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bl = blockIdx.y, b = b0 + bl;
   if (kp.hdr[b].valid == 0) return;  // cold stream (block-uniform)
@@ -239,6 +240,15 @@ __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, 
   const int ya = 2 * pair;
   float2* S = reinterpret_cast<float2*>(smem) + wid * w448::XS;
   const float4* T2 = reinterpret_cast<const float4*>(kp.T2) + ((size_t)bl * 224 + pair) * 224;
+  // the row pair's 3.5 KB T2 block lands in the warp's FFT scratch with one
+  // bulk copy; the lanes then gather their (mirrored) columns from shared memory
+  if (lane == 0) {
+    tma::bar_init(&barc[wid], 1);
+    tma::load_tile(S, T2, 224 * 16, &barc[wid]);
+  }
+  __syncwarp();
+  tma::bar_wait(&barc[wid], 0);
+  const float4* Sb = reinterpret_cast<const float4*>(S);
   const int k1a = lane >> 3, j1 = lane & 7;
   float4 in[2][8];
 #pragma unroll
@@ -248,10 +258,11 @@ __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, 
       for (int j2 = 0; j2 < 8; ++j2) {
         const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
         const int qq = (k == 0 || k == 224) ? 0 : (k < 224 ? k : 448 - k);
-        in[h][j2] = __ldg(T2 + qq);
+        in[h][j2] = Sb[qq];
       }
     }
   }
+  __syncwarp();  // block consumed: S becomes FFT scratch
   W448Tw<LAZY> tw;
   tw.load(kp.tw448, kp.tw64, lane);
   float2 v[2][8], a[2][7];
