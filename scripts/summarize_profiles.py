@@ -61,7 +61,13 @@ def main(tag):
     stalls = [h for h in rh if h.startswith("smsp__average_warps_issue_stalled")]
 
     def g(d, k):
-        return d[rh.index(k)] if k in rh else ""
+        # "" for absent metrics; ncu writes "no data" / "n/a" for some counters
+        v = d[rh.index(k)] if k in rh else ""
+        try:
+            float(v)
+        except ValueError:
+            return ""
+        return v
 
     traffic = {}
     lines = [f"# Round evidence `{tag}` (B200, sm_100a)", "",
