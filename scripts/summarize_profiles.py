@@ -63,6 +63,8 @@ def main(tag):
     def g(d, k):
         # "" for absent metrics; ncu writes "no data" / "n/a" for some counters
         v = d[rh.index(k)] if k in rh else ""
+        if k == "Kernel Name":
+            return v
         try:
             float(v)
         except ValueError:
