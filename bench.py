@@ -1,20 +1,25 @@
 #!/usr/bin/env python
-"""FreqCache select + splice throughput on B200 (BASELINE config 5 per GPU).
+"""FreqCache select + splice throughput on B200 (BASELINE config 5).
 
 One step = one decision (fc_select: luma + block-DCT energy, 2-D FFT, phase
 correlation, entropy budget, top-K) plus the bf16 hidden-state splice
-(fc_splice, 1024 x 1152 per stream) for every stream on this rank.
+(fc_splice_inplace, 1024 x 1152 per stream) for every stream of the job.
 
-Workload per rank (weak scaling, streams sharded with no data-path
-collective): 512 independent streams of 448x448x3 fp32 frames, P=14 (1024
-tokens), adaptive budget, config-2 refresh rule (flush when the patch shift
-exceeds 1), cache/fresh hidden states N(0,1) bf16.  Frames are synthetic
-(paper_2604_24391_b200.synth, torch draw on the GPU, untimed) in a ring of
-24 resident steps (29.6 GB); each step reads 1.23 GB of frames (> L2).
+Workload (config 5 as written): 512 independent streams of 448x448x3 fp32
+frames in total, sharded by stream across the ranks (512 / N per GPU, no
+data-path collective; ``"scaling": "strong"``), P=14 (1024 tokens),
+adaptive budget, config-2 refresh rule (flush when the patch shift exceeds
+1), cache/fresh hidden states N(0,1) bf16.  ``--weak`` keeps 512 streams per
+GPU instead.  Frames are synthetic (paper_2604_24391_b200.synth, torch draw
+on the GPU, untimed) in a ring of 24 resident steps; each step reads
+1.23 GB of frames (> L2).  Each pipelined step (select of step t beside the
+splice of step t - 1) is one CUDA-graph launch.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Prints ONE JSON line on rank 0.
+``--gpus N`` without torchrun re-launches itself under
+``torch.distributed.run`` with N ranks (one per GPU, NCCL).  Prints ONE JSON
+line on rank 0.
 """
 
 from __future__ import annotations
@@ -24,6 +29,7 @@ import json
 
 import numpy as np
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,59 +41,130 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FreqCache select+splice frames/s & tokens/s at 1/2/4/8 B200; % of HBM/TC roofline"
 UNIT = "frames/s"
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=512,
-                    help="streams per rank (weak scaling, default); with --strong: streams of the whole job")
-    ap.add_argument("--strong", action="store_true",
-                    help="config 5 read literally: --streams in total, sharded across the ranks")
+                    help="streams of the whole job (config 5), sharded across the ranks; "
+                         "with --weak: streams per rank")
+    ap.add_argument("--weak", action="store_true", help="--streams per rank instead of in total")
     ap.add_argument("--size", type=int, default=448)
     ap.add_argument("--patch", type=int, default=14)
     ap.add_argument("--dim", type=int, default=1152)
-    ap.add_argument("--ring", type=int, default=24, help="resident frame steps")
+    ap.add_argument("--ring", type=int, default=24, help="resident frame steps (even)")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--sustained-s", type=float, default=1.5,
+                    help="length of the sustained leg (0: skip)")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly")
     ap.add_argument("--cpu-streams", type=int, default=64)
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--cpu-kind", default="auto", choices=["auto", "reference", "port"],
+                    help="CPU baseline: the reference package (baseline/_ref) or the oracle port")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--refresh-shift", type=int, default=1)
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_command(argv, gpus, port):
+    """torchrun command that re-runs this script with one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
 
 
 # ------------------------------------------------------------- CPU legs ----
 
+def reference_available():
+    """The unmodified reference package, installed into baseline/_ref."""
+    if not os.path.isdir(os.path.join(REF_DIR, "freqcache")):
+        return False
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import freqcache  # noqa: F401
+        return os.path.abspath(freqcache.__file__).startswith(os.path.abspath(REF_DIR))
+    except ImportError:
+        return False
+
+
+def _bf16_rows(rng, n, dim):
+    """bf16 N(0,1) rows as their 16-bit patterns (bit copies everywhere)."""
+    return (rng.standard_normal((n, dim), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+
+
 def _cpu_worker(args):
-    """Oracle port on one core: decide + splice for its streams (timed per step)."""
-    streams, steps, warmup, size, patch, dim, refresh_shift, seed = args
+    """One host core: decide + splice for its streams, timed per step.
+
+    kind "reference": the reference's own ``decide`` and ``step``
+    (fusion.py:121-242, 462-512) from baseline/_ref — gray frames by its
+    LUMA_WEIGHTS (frameio.py:26,85-88), hidden states as float64 tokens
+    (bf16 values, exact), fresh rows fed to ``step`` through its token_fn in
+    row-major recompute order, the config-2 shift rule applied on top.
+    kind "port": the oracle restatement (oracle/freqcache_oracle.py)."""
+    kind, streams, steps, warmup, size, patch, dim, refresh_shift, seed = args
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    import numpy as np
-    from oracle import freqcache_oracle as O
+    import dataclasses
     from paper_2604_24391_b200.synth import stream_frames
     n = (size // patch) ** 2
-    cfg = O.OracleConfig(patch_size=patch, refresh_shift=refresh_shift)
     total = warmup + steps + 1
     data = []
     for s in streams:
         fr = stream_frames(seed, s, total, size, size)
         rng = np.random.default_rng([3000, s])
-        # bf16 hidden states ~ N(0,1), kept as their 16-bit patterns (bit copy)
-        cache = (rng.standard_normal((n, dim), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-        fresh = (rng.standard_normal((n, dim), dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
-        data.append((fr, cache, fresh, np.zeros(n, dtype=np.int64)))
+        data.append((fr, _bf16_rows(rng, n, dim), _bf16_rows(rng, n, dim)))
+    if kind == "reference":
+        sys.path.insert(0, REF_DIR)
+        import freqcache as ref
+        from freqcache.frameio import LUMA_WEIGHTS
+        cfg = ref.CacheConfig(patch_size=patch)
+        rows = size // patch
+
+        def gray(rgb):
+            a = rgb.astype(np.float64)
+            return LUMA_WEIGHTS[0] * a[..., 0] + LUMA_WEIGHTS[1] * a[..., 1] + LUMA_WEIGHTS[2] * a[..., 2]
+
+        def bf16_f64(u16):
+            return (u16.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+        state = [ref.TokenCache(bf16_f64(c).reshape(rows, rows, dim), np.zeros((rows, rows), np.int64))
+                 for _, c, _ in data]
+        fresh64 = [bf16_f64(f) for _, _, f in data]
+
+        def one(k, t):
+            fr = data[k][0]
+            d = ref.decide(gray(fr[t - 1]), gray(fr[t]), cfg, step=t)
+            if (refresh_shift is not None and refresh_shift >= 0 and d.diagnostic is None and not d.flushed
+                    and max(abs(d.displacement.di_patches), abs(d.displacement.dj_patches)) > refresh_shift):
+                d = dataclasses.replace(d, flushed=True, k_candidate=0, k_final=0, reuse_set=(),
+                                        recompute_set=tuple(range(n)))
+            rec = iter(fresh64[k][list(d.recompute_set)] if not d.flushed else fresh64[k])
+            state[k], _ = ref.step(state[k], d, gray(fr[t]), lambda patch_: next(rec))
+    else:
+        from oracle import freqcache_oracle as O
+        cfg = O.OracleConfig(patch_size=patch, refresh_shift=refresh_shift)
+        state = [(c, np.zeros(n, dtype=np.int64)) for _, c, _ in data]
+
+        def one(k, t):
+            fr, _, fresh = data[k]
+            d = O.decide(fr[t - 1], fr[t], cfg, step=t)
+            state[k] = O.splice(state[k][0], state[k][1], d, fresh[list(d.recompute_set)])
     t_timed = 0.0
     frames_done = 0
     for t in range(1, total):
         t0 = time.perf_counter()
-        for k, (fr, cache, fresh, ages) in enumerate(data):
-            d = O.decide(fr[t - 1], fr[t], cfg, step=t)
-            rec = list(d.recompute_set)
-            cache2, ages2 = O.splice(cache, ages, d, fresh[rec])
-            data[k] = (fr, cache2, fresh, ages2)
+        for k in range(len(data)):
+            one(k, t)
         dt = time.perf_counter() - t0
         if t > warmup:
             t_timed += dt
@@ -95,7 +172,9 @@ def _cpu_worker(args):
     return frames_done, t_timed
 
 
-def cpu_run(n_streams, steps, warmup, size, patch, dim, refresh_shift, seed=5000):
+def cpu_run(kind, n_streams, steps, warmup, size, patch, dim, refresh_shift, seed=5000):
+    """Whole-host CPU throughput (frames/s): one process per core, BLAS
+    threads 1; returns (frames/s, cores, frames timed)."""
     import multiprocessing as mp
     cores = len(os.sched_getaffinity(0))
     workers = min(cores, n_streams)
@@ -106,7 +185,8 @@ def cpu_run(n_streams, steps, warmup, size, patch, dim, refresh_shift, seed=5000
         os.environ[k] = "1"
     try:
         with ctx.Pool(workers) as pool:
-            res = pool.map(_cpu_worker, [(p, steps, warmup, size, patch, dim, refresh_shift, seed) for p in parts])
+            res = pool.map(_cpu_worker, [(kind, p, steps, warmup, size, patch, dim, refresh_shift, seed)
+                                         for p in parts])
     finally:
         for k, v in env_keep.items():
             if v is None:
@@ -118,29 +198,78 @@ def cpu_run(n_streams, steps, warmup, size, patch, dim, refresh_shift, seed=5000
     return frames / wall if wall > 0 else 0.0, workers, frames
 
 
+def cpu_kind(a):
+    if a.cpu_kind == "port":
+        return "port"
+    ok = reference_available()
+    if a.cpu_kind == "reference" and not ok:
+        raise SystemExit("--cpu-kind reference: baseline/_ref/freqcache is not installed")
+    return "reference" if ok else "port"
+
+
+def cpu_sample_text(kind, streams, steps, warmup, frames):
+    what = ("the reference's own decide + step (baseline/_ref freqcache, unmodified; luma by its "
+            "LUMA_WEIGHTS, fresh rows through its token_fn, config-2 shift rule on top)"
+            if kind == "reference" else "the oracle port (decide + splice)")
+    return (f"{streams} streams x {steps} timed steps (+{warmup} warm-up) of {what}, {frames} frames, numpy "
+            "draw of the same frozen generator, one process per core, BLAS threads 1")
+
+
 def run_reference(a):
-    """--impl reference: the CPU oracle port of the reference path on all host cores."""
+    """--impl reference: the reference's CPU path on all host cores (rank 0)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     t0 = time.time()
-    v, cores, frames = cpu_run(a.cpu_streams, a.steps, a.warmup, a.size, a.patch, a.dim, a.refresh_shift)
+    kind = cpu_kind(a)
+    v, cores, frames = cpu_run(kind, a.cpu_streams, a.steps, a.warmup, a.size, a.patch, a.dim, a.refresh_shift)
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * a.cpu_streams / v if v else None,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if a.weak else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (numpy draw of the frozen generator)",
         "config": {"workload": "config5 sample: decide+splice per frame, 448x448x3 fp32, P=14, N=1024, D=1152",
                    "streams": a.cpu_streams, "size": a.size, "patch": a.patch, "dim": a.dim,
                    "refresh_shift": a.refresh_shift},
         "tokens_per_s": v * (a.size // a.patch) ** 2,
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{a.cpu_streams} streams x {a.steps} steps (+{a.warmup} warm-up) of "
-                                   "oracle decide + splice, one process per core, BLAS threads 1"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": cpu_sample_text(kind, a.cpu_streams, a.steps, a.warmup, frames)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.time() - t0,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_plumbing(a):
+    """FC_BENCH_PLUMBING=1 (CPU tests): the multi-rank launch and reporting
+    path without kernels — gloo ranks, stream sharding, max-over-ranks
+    timing, the counter all-reduce and the rank-0 line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_24391_b200.dist import gather_counters, max_over_ranks, shard
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    total = a.streams * world if a.weak else a.streams
+    lo, hi = shard(total, world, rank)
+    ms = max_over_ranks(1.0 + rank)
+    n = (a.size // a.patch) ** 2
+    cnt = gather_counters({"frames": (hi - lo) * a.steps, "tokens": (hi - lo) * a.steps * n,
+                           "reused_tokens": 0, "flushes": 0, "cold": 0})
+    spans = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(spans, torch.tensor([lo, hi], dtype=torch.int64))
+    else:
+        spans = [torch.tensor([lo, hi])]
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "plumbing": True, "n_gpus": world, "ms_max": ms,
+                          "streams_total": total, "streams_per_rank": [int(s[1] - s[0]) for s in spans],
+                          "spans": [[int(s[0]), int(s[1])] for s in spans], "frames": cnt["frames"],
+                          "scaling": "weak" if a.weak else "strong"}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 # ------------------------------------------------------------- GPU side ----
@@ -186,6 +315,7 @@ class ClockSampler:
         # a sample is read shortly after it is taken: allow about one period
         time.sleep(0.03)
         self.window[1] = time.monotonic()
+        return tuple(self.window)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -195,10 +325,11 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, window=None):
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        lo, hi = self.window if self.window and self.window[1] else (float("-inf"), float("inf"))
+        window = window or self.window
+        lo, hi = window if window and window[1] else (float("-inf"), float("inf"))
         for ts, ln in self.lines:
             if not (lo <= ts <= hi):
                 continue
@@ -247,17 +378,17 @@ def run_ours(a):
         else:
             dist.init_process_group(backend)
 
-    from paper_2604_24391_b200 import CacheConfig, FreqCacheEngine, SpliceState
+    from paper_2604_24391_b200 import CacheConfig, FreqCacheEngine, SpliceState, StepGraph
     from paper_2604_24391_b200.synth import torch_stream_frames
 
-    S, H, P, D, R = a.streams, a.size, a.patch, a.dim, a.ring
-    total_streams = S if a.strong else S * world
+    H, P, D, R = a.size, a.patch, a.dim, a.ring + (a.ring & 1)
+    total_streams = a.streams * world if a.weak else a.streams
     N = (H // P) ** 2
     cfg = CacheConfig(patch_size=P)
 
     # ---- inputs, resident in HBM before timing (untimed generation); this
-    # rank's streams are its contiguous block of the job's S * world streams
-    from paper_2604_24391_b200.dist import gather_counters, shard, step_counters
+    # rank's streams are its contiguous block of the job's streams
+    from paper_2604_24391_b200.dist import gather_counters, shard
     lo, hi = shard(total_streams, world, rank)
     S = hi - lo
     frames = torch.empty((R, S, H, H, 3), dtype=torch.float32, device=dev)
@@ -273,66 +404,54 @@ def run_ours(a):
     ages = torch.zeros((2, S, N), dtype=torch.int64, device=dev)
     eng = FreqCacheEngine(S, H, H, P, fmt="rgb", device=dev)
     spl = SpliceState(cache, ages)   # in place where the displacement is zero, else ping-pong
+    # run_sequence aggregates over the timed steps, accumulated by the select
+    # kernel itself (frames, reused tokens, flushes, cold)
+    counters = torch.zeros(4, dtype=torch.int64, device=dev)
+    outs = [eng.out, eng.new_output()]
+    for o in outs:
+        o.counters = counters
     torch.cuda.synchronize()
 
-    cur = [0]
     launches = [0]
-
-    # Pipelined steps: select(t) on the main stream, splice(t) on a second
-    # stream, so the HBM-bound splice of step t overlaps the FFT-bound select
-    # of step t+1.  Select outputs are double-buffered; splice(t-2) must have
-    # consumed a buffer before select(t) rewrites it.
+    per_phase = eng.launches_per_select + 2   # + splice plan + copier
     main = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_SIDE_PRIO", "-1")))  # splice CTAs jump the select queue
-    outs = [eng.out, eng.new_output()]
-    sel_ev = [torch.cuda.Event(), torch.cuda.Event()]
-    spl_ev = [torch.cuda.Event(), torch.cuda.Event()]
-    for e in spl_ev:
-        e.record(main)
+    n_spliced = [0]   # splices issued so far: SpliceState's ping-pong parity
 
-    def pipe_step(t):
+    def phase(t):
+        """Pipelined step t on the current stream: select(t) beside the
+        splice of step t - 1 (forked onto the high-priority side stream and
+        joined at the end).  Select outputs are double-buffered, so select(t)
+        rewrites the buffer splice(t - 2) read one step earlier."""
+        cur = torch.cuda.current_stream(dev)
+        side.wait_stream(cur)
+        eng.select(frames[t % R], cfg, out=outs[t & 1], refresh_shift=a.refresh_shift)
+        if t > 0:
+            with torch.cuda.stream(side):
+                spl.step(outs[(t - 1) & 1].src_map, fresh)
+            n_spliced[0] += 1
+            cur.wait_stream(side)
+
+    def one_step(t, kernel_ms):
+        """Serial select + splice with per-kernel timing (events between launches)."""
         fr = frames[t % R]
-        k = t & 1
-        main.wait_event(spl_ev[k])
-        out = eng.select(fr, cfg, out=outs[k], refresh_shift=a.refresh_shift)
-        sel_ev[k].record(main)
-        launches[0] += eng.launches_per_select
-        with torch.cuda.stream(side):
-            side.wait_event(sel_ev[k])
-            spl.step(out.src_map, fresh)
-            spl_ev[k].record(side)
-        launches[0] += 2
-        return out
-
-    def drain():
-        for e in spl_ev:
-            main.wait_event(e)
-
-    def one_step(t, kernel_ms=None):
-        fr = frames[t % R]
-        if kernel_ms is None:
-            out = eng.select(fr, cfg, refresh_shift=a.refresh_shift)
-        else:
-            prof = []
-            out = eng.select(fr, cfg, refresh_shift=a.refresh_shift, profile=prof)
-            for k in range(4):
-                kernel_ms[k] += prof[k]
-        launches[0] += eng.launches_per_select
-        if kernel_ms is not None:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+        prof = []
+        out = eng.select(fr, cfg, refresh_shift=a.refresh_shift, profile=prof)
+        for k in range(4):
+            kernel_ms[k] += prof[k]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         spl.step(out.src_map, fresh)
-        if kernel_ms is not None:
-            e1.record()
-            torch.cuda.synchronize()
-            kernel_ms[4] += e0.elapsed_time(e1)
-            # bytes the splice actually moves this step: in-place streams only
-            # their recomputed rows, shifted streams every row
-            r = out.host_results()
-            moved = ((r["k_final"] > 0) & ((r["di_patches"] != 0) | (r["dj_patches"] != 0)))
-            rows_moved = np.where(moved, N, N - r["k_final"]).sum()
-            splice_bytes[0] += int(rows_moved) * 2 * D * 2 + S * 20 * N
-        launches[0] += 2
+        n_spliced[0] += 1
+        e1.record()
+        torch.cuda.synchronize()
+        kernel_ms[4] += e0.elapsed_time(e1)
+        # bytes the splice actually moves this step: in-place streams only
+        # their recomputed rows, shifted streams every row
+        r = out.host_results()
+        moved = ((r["k_final"] > 0) & ((r["di_patches"] != 0) | (r["dj_patches"] != 0)))
+        rows_moved = np.where(moved, N, N - r["k_final"]).sum()
+        splice_bytes[0] += int(rows_moved) * 2 * D * 2 + S * 20 * N
         return out
 
     def barrier():
@@ -340,34 +459,82 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # ---- one CUDA graph per ring phase (frames[t % R], outs[t & 1] and the
+    # splice ping-pong parity repeat with period R)
+    graphs = None
+    phase(0)                                   # step 0 establishes every stream's spectrum
+    t_next = 1
+    if not a.no_graph:
+        base = n_spliced[0]
+        graphs = []
+        for p in range(R):
+            t = t_next + p
+            spl.k = (base + (t - 1)) & 1      # the parity splice(t - 1) has at replay
+            graphs.append(StepGraph(lambda t=t: phase(t), device=dev))
+        n_spliced[0] = base
+        spl.k = base & 1
+        torch.cuda.synchronize()
+
+    def run(t):
+        if graphs is None:
+            phase(t)
+        else:
+            graphs[(t - 1) % R].replay()
+            n_spliced[0] += 1
+            spl.k = n_spliced[0] & 1
+        launches[0] += per_phase
+
     # clock sampling starts before the warm-up, so the GPU does not idle while
     # nvidia-smi starts; only samples inside the timed region are kept
     clocks = ClockSampler(local).__enter__()
-    # ---- warm-up (step 0 establishes every stream's spectrum)
-    w0 = a.warmup
-    for t in range(w0):
-        pipe_step(t)
-    drain()
+    # ---- warm-up: step 0 (above) + W - 1 pipelined steps
+    for _ in range(max(0, a.warmup - 1)):
+        run(t_next)
+        t_next += 1
     barrier()
 
-    # ---- timed region: K steps, CUDA events on the launching stream
+    # ---- timed region: K pipelined steps (K selects beside K splices), CUDA
+    # events on the launching stream, max over ranks
     stream = torch.cuda.current_stream(dev)
+    counters.zero_()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches[0] = 0
+    sustained = None
     try:
         barrier()
         clocks.start()
         ev0.record(stream)
-        for t in range(w0, w0 + a.steps):
-            pipe_step(t)
-        drain()
+        for _ in range(a.steps):
+            run(t_next)
+            t_next += 1
         ev1.record(stream)
         barrier()
-        clocks.stop()
+        win_main = clocks.stop()
+        gpu_launches = launches[0]
+        ms = ev0.elapsed_time(ev1)
+        cnt_dev = counters.clone()
+        # ---- sustained leg: the same steps for >= --sustained-s seconds, with
+        # its own clock record (the short default region runs at burst clocks)
+        if a.sustained_s > 0:
+            n_s = max(a.steps, int(a.sustained_s * 1e3 / max(ms / a.steps, 1e-3)) + 1)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            clocks.start()
+            s0.record(stream)
+            for _ in range(n_s):
+                run(t_next)
+                t_next += 1
+            s1.record(stream)
+            barrier()
+            win_s = clocks.stop()
+            sms = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(sms, op=dist.ReduceOp.MAX)
+            sms = float(sms.item())
+            sustained = {"value": total_streams * n_s / (sms / 1e3), "unit": UNIT, "steps": n_s,
+                         "seconds": sms / 1e3, "ms_per_step": sms / n_s, "clocks": clocks.summary(win_s)}
     finally:
         clocks.__exit__(None, None, None)
-    gpu_launches = launches[0]
-    ms = ev0.elapsed_time(ev1)
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
@@ -375,20 +542,26 @@ def run_ours(a):
     frames_total = total_streams * a.steps
     value = frames_total / (ms / 1e3)
 
-    # decision statistics of the last timed step over all ranks (the only
-    # other collective: a few counters, NCCL all-reduce over NVLink)
-    res = outs[(w0 + a.steps - 1) & 1].host_results()
-    cnt = gather_counters(step_counters(res), device=dev)
-    reuse_ratio = cnt["reused_tokens"] / cnt["tokens"]
-    flush_rate = cnt["flushes"] / cnt["frames"]
+    # decision statistics over every timed step of every rank (the only other
+    # collective: a few counters, NCCL all-reduce over NVLink)
+    c = cnt_dev.cpu().tolist()
+    cnt = gather_counters({"frames": c[0], "tokens": c[0] * N, "reused_tokens": c[1], "flushes": c[2],
+                           "cold": c[3]}, device=dev)
+    reuse_ratio = cnt["reused_tokens"] / max(cnt["tokens"], 1)
+    flush_rate = cnt["flushes"] / max(cnt["frames"], 1)
+
+    # complete the last pipelined step's splice, then the serial pass
+    spl.step(outs[(t_next - 1) & 1].src_map, fresh)
+    n_spliced[0] += 1
+    torch.cuda.synchronize()
 
     # ---- per-kernel timing pass (same steps, events between launches)
     kp_steps = min(a.steps, 16)
     names = ["rows_fwd", "cols", "rows_inv", "select", "splice"]
     kms = [0.0] * 5
-    t0 = w0 + a.steps
+    t0 = t_next
     for t in range(t0, t0 + kp_steps):
-        one_step(t, kernel_ms=kms)
+        one_step(t, kms)
     kms = [v / kp_steps for v in kms]
     splice_moved = splice_bytes[0] / kp_steps
     hw = H * H
@@ -551,20 +724,21 @@ def run_ours(a):
     # ---- CPU baseline (rank 0, N == 1 only)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        v, cores, nfr = cpu_run(a.cpu_streams, a.cpu_steps, 1, H, P, D, a.refresh_shift)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{a.cpu_streams} streams x {a.cpu_steps} timed steps of the oracle port "
-                         f"(decide + splice, {nfr} frames), numpy draw of the same generator, "
-                         "one process per core, BLAS threads 1"}
+        kind = cpu_kind(a)
+        v, cores, nfr = cpu_run(kind, a.cpu_streams, a.cpu_steps, 1, H, P, D, a.refresh_shift)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": cpu_sample_text(kind, a.cpu_streams, a.cpu_steps, 1, nfr)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
-            "scaling": "strong" if a.strong else "weak",
+            "scaling": "weak" if a.weak else "strong",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (frozen generator, torch draw on GPU; cache/fresh bf16 N(0,1))",
-            "config": {"workload": "config5 per GPU: select + splice, adaptive budget, refresh on shift>1",
+            "config": {"workload": (f"config5 {'weak: ' + str(a.streams) + ' streams per GPU' if a.weak else 'as written: ' + str(total_streams) + ' streams in total, ' + str(S) + ' per GPU'}"
+                                    ": select + splice, adaptive budget, refresh on shift>1"),
+                       "graph": not a.no_graph,
                        "streams_per_gpu": S, "streams_total": total_streams, "size": H, "channels": 3, "patch": P, "tokens": N,
                        "hidden": D, "hidden_dtype": "bf16", "frame_ring_steps": R,
                        "l2": f"inputs > L2 ({S * H * H * 12 / 1e9:.2f} GB of frames per step, "
@@ -583,8 +757,10 @@ def run_ours(a):
             "gpu_launches": gpu_launches,
             "latency": latency,
             "clocks": clocks.summary(),
-            "decisions": {"reuse_ratio_last_step": reuse_ratio, "flush_rate_last_step": flush_rate,
-                          "streams_last_step": int(cnt["frames"])},
+            "decisions": {"reuse_ratio": reuse_ratio, "flush_rate": flush_rate,
+                          "frames": int(cnt["frames"]), "cold": int(cnt["cold"]),
+                          "over": "every timed step of every rank (select-kernel counters)"},
+            "sustained": sustained,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -594,7 +770,21 @@ def run_ours(a):
 
 def main():
     a = parse()
-    if a.impl == "reference":
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and a.gpus > 1:
+        # one process per GPU: re-run this script under torchrun with N ranks
+        # (the reference arm is CPU-only and runs on rank 0 alone, so it needs
+        # no ranks)
+        if a.impl == "reference":
+            run_reference(a)
+            return
+        sys.exit(subprocess.call(launch_command(sys.argv[1:], a.gpus, free_port())))
+    if ws is not None and int(ws) != a.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={ws} but --gpus {a.gpus}; refusing the mismatch\n")
+        sys.exit(2)
+    if os.environ.get("FC_BENCH_PLUMBING") == "1":
+        run_plumbing(a)
+    elif a.impl == "reference":
         run_reference(a)
     else:
         run_ours(a)

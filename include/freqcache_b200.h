@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define FC_ABI_VERSION 1
+#define FC_ABI_VERSION 2  /* 2: splice entry points take a status word */
 
 /* status codes (fc_strerror) */
 #define FC_OK            0
@@ -116,6 +116,11 @@ typedef struct fc_select_out {
   uint8_t* reuse_mask;       /* [B][N]                                        */
   uint8_t* refresh_mask;     /* [B][N]                                        */
   double*  energy;           /* [B][N] high-pass DCT energy                   */
+  int64_t* counters;         /* optional [4], accumulated (integer atomics):
+                                frames, reused tokens (sum k_final), flushes
+                                of warm streams, cold streams — the
+                                run_sequence aggregates (fusion.py:559-572);
+                                NULL to skip                                 */
 } fc_select_out;
 
 typedef struct fc_plan fc_plan;
@@ -159,12 +164,17 @@ int  fc_patch_energy(const fc_plan* plan, const void* frames, void* workspace,
  * out_ages likewise (cache_ages+1 / 0).  cache may be NULL when every entry
  * of src_map is negative.  row_bytes = D * element size (any, bit copy).
  * fresh_rows: rows per stream in `fresh` (ignored for FC_FRESH_DENSE, where
- * it is n_tokens; for FC_FRESH_COMPACT any capacity >= the recompute count). */
+ * it is n_tokens; for FC_FRESH_COMPACT any capacity >= the recompute count).
+ * status (device int32, may be NULL; the caller zeroes it): every splice
+ * kernel checks each row's source as fusion.py:488-490 asserts it — a cache
+ * source outside [0, n_tokens) (or any cache source with cache == NULL), or
+ * a compact fresh index >= fresh_rows — skips that row and stores
+ * FC_EBOUNDS in *status (the facade raises AssertionError).                 */
 int  fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                const int32_t* src_map, const void* cache,
                const int64_t* cache_ages, const void* fresh,
                int32_t fresh_layout, int32_t fresh_rows, void* out,
-               int64_t* out_ages, void* cuda_stream);
+               int64_t* out_ages, int32_t* status, void* cuda_stream);
 
 /* Decision mask images (frameio.py:188-219): img[b][p] = 255 reused, 128
  * edge-forced recompute, 0 otherwise; flushed or cold streams all 0.        */
@@ -201,7 +211,7 @@ int  fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                       const int32_t* src_map, const void* cache,
                       const int64_t* cache_ages, const void* fresh,
                       const int64_t* fresh_offsets, void* out, int64_t* out_ages,
-                      void* cuda_stream);
+                      int32_t* status, void* cuda_stream);
 
 /* In-place splice over a per-stream ping-pong pair of caches.  slot_in[b]
  * (device u8) names the buffer (0/1) holding stream b's cache.  A stream whose
@@ -214,7 +224,8 @@ int  fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                        const int32_t* src_map, void* cache0, void* cache1,
                        int64_t* ages0, int64_t* ages1, const uint8_t* slot_in,
                        uint8_t* slot_out, const void* fresh, int32_t fresh_layout,
-                       int32_t fresh_rows, void* scratch, void* cuda_stream);
+                       int32_t fresh_rows, void* scratch, int32_t* status,
+                       void* cuda_stream);
 
 /* Build src_map for one stream from an ordered reuse list (fusion.py:481-504).
  * flag (device int32, may be NULL) receives FC_EBOUNDS on an out-of-bounds
@@ -236,6 +247,15 @@ int  fc_compare_cosines(const fc_geometry* geom, const void* prev, const void* c
  * custom token_fn's vectors.                                                */
 int  fc_row_cosines(int64_t n, int64_t d, const double* a, const double* b,
                     double* out, void* cuda_stream);
+
+/* ---- CUDA-graph capture of whole steps (runtime plumbing, not an op of the
+ * reference).  Capture everything a step launches on `cuda_stream` (other
+ * streams join through events), instantiate it with per-node priorities and
+ * replay it with one launch per step.                                       */
+int  fc_graph_capture_begin(void* cuda_stream);
+int  fc_graph_capture_end(void* cuda_stream, void** graph_exec);
+int  fc_graph_launch(void* graph_exec, void* cuda_stream);
+void fc_graph_destroy(void* graph_exec);
 
 #ifdef __cplusplus
 }

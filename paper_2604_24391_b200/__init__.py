@@ -52,5 +52,5 @@ from .api import (  # noqa: F401
     step,
     topk_ascending,
 )
-from .engine import FreqCacheEngine, SelectResult, SpliceState, splice, splice_map  # noqa: F401
+from .engine import FreqCacheEngine, SelectResult, SpliceState, StepGraph, splice, splice_map  # noqa: F401
 from . import records  # noqa: F401

@@ -46,6 +46,7 @@ EXPORTS = (
     "fc_splice_map", "fc_stage_workspace_bytes", "fc_amp_cosine", "fc_spectral_sums",
     "fc_refresh_mask", "fc_topk_ascending", "fc_render_masks", "fc_splice_packed",
     "fc_splice_inplace", "fc_splice_inplace_scratch_bytes", "fc_compare_cosines", "fc_row_cosines",
+    "fc_graph_capture_begin", "fc_graph_capture_end", "fc_graph_launch", "fc_graph_destroy",
 )
 
 
@@ -64,7 +65,7 @@ class SelectOut(C.Structure):
     _fields_ = [("results", C.c_void_p), ("reuse_idx", C.c_void_p),
                 ("recompute_idx", C.c_void_p), ("src_map", C.c_void_p),
                 ("reuse_mask", C.c_void_p), ("refresh_mask", C.c_void_p),
-                ("energy", C.c_void_p)]
+                ("energy", C.c_void_p), ("counters", C.c_void_p)]
 
 
 # fc_stream_result as a numpy structured dtype (identical layout)
@@ -112,12 +113,12 @@ def load(path=None):
         "fc_select_profile": (C.c_int, [vp, C.POINTER(Config), vp, vp, vp, C.POINTER(SelectOut),
                                         C.POINTER(C.c_float), vp]),
         "fc_patch_energy": (C.c_int, [vp, vp, vp, vp, vp]),
-        "fc_splice": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
+        "fc_splice": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp]),
         "fc_splice_map": (C.c_int, [i32, i32, vp, i32, i32, i32, vp, vp, vp]),
         "fc_stage_workspace_bytes": (i64, []),
         "fc_render_masks": (C.c_int, [i32, i32, vp, vp, vp, vp, vp]),
-        "fc_splice_packed": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
-        "fc_splice_inplace": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]),
+        "fc_splice_packed": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "fc_splice_inplace": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
         "fc_splice_inplace_scratch_bytes": (i64, [i32, i32]),
         "fc_amp_cosine": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
         "fc_spectral_sums": (C.c_int, [vp, i64, i32, vp, vp, vp, vp]),
@@ -125,6 +126,10 @@ def load(path=None):
         "fc_topk_ascending": (C.c_int, [vp, i64, vp, i64, i64, vp, vp, vp]),
         "fc_compare_cosines": (C.c_int, [C.POINTER(Geometry), vp, vp, vp, vp, vp]),
         "fc_row_cosines": (C.c_int, [i64, i64, vp, vp, vp, vp]),
+        "fc_graph_capture_begin": (C.c_int, [vp]),
+        "fc_graph_capture_end": (C.c_int, [vp, C.POINTER(vp)]),
+        "fc_graph_launch": (C.c_int, [vp, vp]),
+        "fc_graph_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -550,6 +550,9 @@ int fc_select_profile(const fc_plan* pl, const fc_config* cfg, const void* frame
 
 int fc_patch_energy(const fc_plan* pl, const void* frames, void* ws, double* energy, void* stream) {
   if (!pl || !frames || !ws || !energy) return FC_EINVAL;
+  // the 448 path bulk-copies frame stripes (16-byte aligned sources), as fc_select
+  if (((pl->fast ? reinterpret_cast<uintptr_t>(frames) : 0) | reinterpret_cast<uintptr_t>(ws)) & 15)
+    return FC_EINVAL;
   const KParams kp = bind(pl, nullptr, ws, energy);
   const cudaStream_t st = as_stream(stream);
   if (pl->fast) {
@@ -567,7 +570,7 @@ int fc_patch_energy(const fc_plan* pl, const void* frames, void* ws, double* ene
 static int splice_impl(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map,
                        const void* cache, const int64_t* cache_ages, const void* fresh, int compact,
                        int32_t fresh_rows, const int64_t* fresh_off, void* out, int64_t* out_ages,
-                       cudaStream_t st) {
+                       int32_t* status, cudaStream_t st) {
   const int total = batch * n_tokens;
   const bool vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(cache) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(fresh) & 15) == 0) &&
@@ -584,37 +587,58 @@ static int splice_impl(int32_t batch, int32_t n_tokens, int64_t row_bytes, const
     k_splice16<UNR><<<blocks, FC_THREADS, 0, st>>>(
         total, n_tokens, row_bytes / 16, src_map, reinterpret_cast<const int4*>(cache), cache_ages,
         reinterpret_cast<const int4*>(fresh), compact, fresh_rows, fresh_off, reinterpret_cast<int4*>(out),
-        out_ages);
+        out_ages, status);
   } else {
     k_splice_bytes<<<total, 128, 0, st>>>(total, n_tokens, row_bytes, src_map,
                                           reinterpret_cast<const uint8_t*>(cache), cache_ages,
                                           reinterpret_cast<const uint8_t*>(fresh), compact, fresh_rows, fresh_off,
-                                          reinterpret_cast<uint8_t*>(out), out_ages);
+                                          reinterpret_cast<uint8_t*>(out), out_ages, status);
   }
   return launch_check();
 }
 
 int fc_splice(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, const void* cache,
               const int64_t* cache_ages, const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* out,
-              int64_t* out_ages, void* stream) {
+              int64_t* out_ages, int32_t* status, void* stream) {
   if (batch < 1 || n_tokens < 1 || row_bytes < 1 || !src_map || !fresh || !out || !out_ages) return FC_EINVAL;
   if ((int64_t)batch * n_tokens > INT32_MAX) return FC_EINVAL;
   if (fresh_layout != FC_FRESH_DENSE && fresh_layout != FC_FRESH_COMPACT) return FC_EINVAL;
   if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
   if (fresh_rows < 1) return FC_EINVAL;
   return splice_impl(batch, n_tokens, row_bytes, src_map, cache, cache_ages, fresh,
-                     fresh_layout == FC_FRESH_COMPACT, fresh_rows, nullptr, out, out_ages, as_stream(stream));
+                     fresh_layout == FC_FRESH_COMPACT, fresh_rows, nullptr, out, out_ages, status, as_stream(stream));
 }
 
 int fc_splice_packed(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map,
                      const void* cache, const int64_t* cache_ages, const void* fresh,
-                     const int64_t* fresh_offsets, void* out, int64_t* out_ages, void* stream) {
+                     const int64_t* fresh_offsets, void* out, int64_t* out_ages, int32_t* status, void* stream) {
   if (batch < 1 || n_tokens < 1 || row_bytes < 1 || !src_map || !fresh || !fresh_offsets || !out || !out_ages)
     return FC_EINVAL;
   if ((int64_t)batch * n_tokens > INT32_MAX) return FC_EINVAL;
-  return splice_impl(batch, n_tokens, row_bytes, src_map, cache, cache_ages, fresh, 1, 0, fresh_offsets, out,
-                     out_ages, as_stream(stream));
+  // a packed stream holds at most n_tokens recomputed rows
+  return splice_impl(batch, n_tokens, row_bytes, src_map, cache, cache_ages, fresh, 1, n_tokens, fresh_offsets, out,
+                     out_ages, status, as_stream(stream));
 }
+
+}  // extern "C"
+
+using BulkFn = decltype(&k_splice_ip_bulk<2, 2>);
+// Every (lanes, slots) instance the copier can be asked for: the caller sizes
+// dynamic shared memory for exactly this NL and SL.
+template <int NL>
+static BulkFn pick_bulk_sl(int SL) {
+  return SL == 4 ? k_splice_ip_bulk<NL, 4> : SL == 3 ? k_splice_ip_bulk<NL, 3> : k_splice_ip_bulk<NL, 2>;
+}
+static BulkFn pick_bulk(int NL, int SL) {
+  switch (NL) {
+    case 2: return pick_bulk_sl<2>(SL);
+    case 4: return pick_bulk_sl<4>(SL);
+    case 8: return pick_bulk_sl<8>(SL);
+    default: return pick_bulk_sl<16>(SL);
+  }
+}
+
+extern "C" {
 
 int64_t fc_splice_inplace_scratch_bytes(int32_t batch, int32_t n_tokens) {
   return (int64_t)batch * n_tokens * 4 + (int64_t)batch * 4 + 256;
@@ -622,7 +646,8 @@ int64_t fc_splice_inplace_scratch_bytes(int32_t batch, int32_t n_tokens) {
 
 int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, void* cache0,
                       void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in, uint8_t* slot_out,
-                      const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* scratch, void* stream) {
+                      const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* scratch, int32_t* status,
+                      void* stream) {
   if (batch < 1 || n_tokens < 1 || row_bytes < 16 || row_bytes % 16 || !src_map || !cache0 || !cache1 || !ages0 ||
       !ages1 || !slot_in || !slot_out || !fresh || !scratch)
     return FC_EINVAL;
@@ -643,22 +668,19 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
   // Bulk (TMA) copier unless disabled (FC_SPLICE_BULK=0) or the rows/batch do
   // not fit its shared-memory slots.
   // lanes per copier CTA: the compiled variants are 2, 4, 8 and 16
-  static const int NLreq = env_int("FC_SPLICE_BULK_NL", 8, 2, 16);
-  static const int NL = NLreq <= 2 ? 2 : NLreq <= 4 ? 4 : NLreq <= 8 ? 8 : 16;
-  static const int SL = env_int("FC_SPLICE_BULK_SLOTS", 2, 2, 4);
+  const int NLreq = env_int("FC_SPLICE_BULK_NL", 8, 2, 16);
+  const int NL = NLreq <= 2 ? 2 : NLreq <= 4 ? 4 : NLreq <= 8 ? 8 : 16;
+  const int SL = env_int("FC_SPLICE_BULK_SLOTS", 2, 2, 4);
   const size_t bulk_smem = (size_t)NL * SL * row_bytes + (size_t)(batch + 1) * 4;
-  static const int use_bulk = env_int("FC_SPLICE_BULK", 1, 0, 1);
+  const int use_bulk = env_int("FC_SPLICE_BULK", 1, 0, 1);
   if (use_bulk && bulk_smem <= 96 * 1024) {
-    static const int per_sm = env_int("FC_SPLICE_BULK_CTAS", 2, 1, 32);
-    auto fn = SL == 3 ? (NL == 4 ? k_splice_ip_bulk<4, 3> : NL == 8 ? k_splice_ip_bulk<8, 3> : k_splice_ip_bulk<16, 3>)
-            : SL == 4 ? (NL == 4 ? k_splice_ip_bulk<4, 4> : NL == 8 ? k_splice_ip_bulk<8, 4> : k_splice_ip_bulk<16, 4>)
-            : NL == 2 ? k_splice_ip_bulk<2> : NL == 4 ? k_splice_ip_bulk<4> : NL == 8 ? k_splice_ip_bulk<8>
-                                                                                 : k_splice_ip_bulk<16>;
+    const int per_sm = env_int("FC_SPLICE_BULK_CTAS", 2, 1, 32);
+    auto fn = pick_bulk(NL, SL);  // the (NL, SL) instance bulk_smem was sized for
     if (bulk_smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem);
     fn<<<sms * per_sm, 32, bulk_smem, st>>>(
         batch, n_tokens, (int)row_bytes, src_map, reinterpret_cast<char*>(cache0), reinterpret_cast<char*>(cache1),
         ages0, ages1, slot_in, slot_out, rows, counts, reinterpret_cast<const char*>(fresh),
-        fresh_layout == FC_FRESH_COMPACT, fresh_rows);
+        fresh_layout == FC_FRESH_COMPACT, fresh_rows, status);
     return launch_check();
   }
   const int total = batch * n_tokens;
@@ -668,7 +690,7 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
   k_splice_ip<UNR><<<blocks, FC_THREADS, 0, st>>>(
       total, n_tokens, row_bytes / 16, src_map, reinterpret_cast<int4*>(cache0), reinterpret_cast<int4*>(cache1),
       ages0, ages1, slot_in, slot_out, rows, counts, reinterpret_cast<const int4*>(fresh),
-      fresh_layout == FC_FRESH_COMPACT, fresh_rows);
+      fresh_layout == FC_FRESH_COMPACT, fresh_rows, status);
   return launch_check();
 }
 
@@ -720,6 +742,45 @@ int fc_splice_map(int32_t rows, int32_t cols, const int32_t* reuse_idx, int32_t 
   }
   k_splice_map<<<1, 512, smem, as_stream(stream)>>>(rows, cols, reuse_idx, k, dip, djp, src_map, flag);
   return launch_check();
+}
+
+// ------------------------------------------------------------ CUDA graphs ----
+// A whole pipelined step (select of step t beside the splice of step t - 1,
+// forked onto a second stream) is captured once per ring phase and replayed,
+// so the per-step host work is one graph launch.  Instantiated with node
+// priorities so the splice branch keeps its stream's (higher) priority.
+
+int fc_graph_capture_begin(void* stream) {
+  return cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal) == cudaSuccess ? FC_OK
+                                                                                                    : FC_ECUDA;
+}
+
+int fc_graph_capture_end(void* stream, void** exec) {
+  if (!exec) return FC_EINVAL;
+  *exec = nullptr;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamEndCapture(as_stream(stream), &g) != cudaSuccess || !g) {
+    cudaGetLastError();
+    return FC_ECUDA;
+  }
+  cudaGraphExec_t ge = nullptr;
+  const cudaError_t e = cudaGraphInstantiateWithFlags(&ge, g, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return FC_ECUDA;
+  }
+  *exec = ge;
+  return FC_OK;
+}
+
+int fc_graph_launch(void* exec, void* stream) {
+  if (!exec) return FC_EINVAL;
+  return cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), as_stream(stream)) == cudaSuccess ? FC_OK : FC_ECUDA;
+}
+
+void fc_graph_destroy(void* exec) {
+  if (exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
 }
 
 // --------------------------------------------------------- mask images ----

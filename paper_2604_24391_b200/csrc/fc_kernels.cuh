@@ -942,9 +942,30 @@ __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_sel
     }
   }
   if (threadIdx.x == 0 && out.results) out.results[b] = R;
+  if (threadIdx.x == 0 && out.counters) {
+    // run_sequence aggregates (fusion.py:559-572): integer atomics, so the
+    // totals are exact and order-independent
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(out.counters);
+    atomicAdd(c + 0, 1ull);
+    atomicAdd(c + 1, (unsigned long long)R.k_final);
+    atomicAdd(c + 2, (unsigned long long)(R.flushed && !R.cold));
+    atomicAdd(c + 3, (unsigned long long)R.cold);
+  }
 }
 
 // ----------------------------------------------------------------- K_E ----
+
+// Splice source check (fusion.py:488-490): a cache source must name a token
+// of the stream's grid, a compact fresh index a row the caller supplied.  A
+// bad row is skipped and FC_EBOUNDS is left in *status (all writers store the
+// same value, so plain stores suffice).
+__device__ __forceinline__ bool splice_src_ok(int s, int n_tokens, bool have_cache, int compact, int fresh_rows) {
+  if (s >= 0) return have_cache && s < n_tokens;
+  return !compact || (-(s + 1)) < fresh_rows;
+}
+__device__ __forceinline__ void flag_bounds(int32_t* status) {
+  if (status) *reinterpret_cast<volatile int32_t*>(status) = FC_EBOUNDS;
+}
 
 // Hidden-state splice (fusion.py:462-512): one warp per token row, 16-byte
 // vector copies, UNR rows in flight per warp.  Bit copy of any dtype.
@@ -956,7 +977,8 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice16(int total, int n_tokens
                                                          const int4* __restrict__ fresh, int compact,
                                                          int fresh_rows, const int64_t* __restrict__ fresh_off,
                                                          int4* __restrict__ out,
-                                                         int64_t* __restrict__ out_ages) {
+                                                         int64_t* __restrict__ out_ages,
+                                                         int32_t* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -967,13 +989,19 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice16(int total, int n_tokens
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int row = r0 + u;
-      on[u] = row < total;
-      const int rr = on[u] ? row : r0;
+      const int rr = row < total ? row : r0;
       const int bs = rr / n_tokens;
       const int s = src_map[rr];
       const size_t base = (size_t)bs * n_tokens;
-      if (s >= 0) src[u] = cache + (base + s) * row16;
-      else {
+      // fusion.py:488-490 asserts the reuse source lies inside the grid
+      const bool ok = splice_src_ok(s, n_tokens, cache != nullptr, compact, fresh_rows);
+      on[u] = row < total && ok;
+      if (row < total && !ok && lane == 0) flag_bounds(status);
+      if (!ok) {
+        src[u] = fresh;
+      } else if (s >= 0) {
+        src[u] = cache + (base + s) * row16;
+      } else {
         const size_t row0 = fresh_off ? (size_t)fresh_off[bs] : (size_t)bs * fresh_rows;
         src[u] = fresh + (row0 + (compact ? (-s - 1) : (rr - bs * n_tokens))) * row16;
       }
@@ -1006,12 +1034,16 @@ __global__ void k_splice_bytes(int total, int n_tokens, int64_t row_bytes, const
                                const uint8_t* __restrict__ cache, const int64_t* __restrict__ cache_ages,
                                const uint8_t* __restrict__ fresh, int compact, int fresh_rows,
                                const int64_t* __restrict__ fresh_off, uint8_t* __restrict__ out,
-                               int64_t* __restrict__ out_ages) {
+                               int64_t* __restrict__ out_ages, int32_t* __restrict__ status) {
   const int row = blockIdx.x;
   if (row >= total) return;
   const int bs = row / n_tokens;
   const int s = src_map[row];
   const size_t base = (size_t)bs * n_tokens;
+  if (!splice_src_ok(s, n_tokens, cache != nullptr, compact, fresh_rows)) {
+    if (threadIdx.x == 0) flag_bounds(status);
+    return;
+  }
   const uint8_t* src = s >= 0 ? cache + (base + s) * row_bytes
                               : fresh + ((fresh_off ? (size_t)fresh_off[bs] : (size_t)bs * fresh_rows) +
                                          (compact ? (-s - 1) : (row - bs * n_tokens))) * row_bytes;
@@ -1140,7 +1172,7 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice_ip(int total, int n_token
                                                           const int32_t* __restrict__ rows,
                                                           const int32_t* __restrict__ counts,
                                                           const int4* __restrict__ fresh, int compact,
-                                                          int fresh_rows) {
+                                                          int fresh_rows, int32_t* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -1160,6 +1192,11 @@ __global__ void __launch_bounds__(FC_THREADS) k_splice_ip(int total, int n_token
       const size_t base = (size_t)bs * n_tokens;
       const int p = rows[base + k];
       const int s = src_map[base + p];
+      if (!splice_src_ok(s, n_tokens, true, compact, fresh_rows)) {
+        if (lane == 0) flag_bounds(status);
+        on[u] = false;
+        continue;
+      }
       const int cur = slot_in[bs], nxt = slot_out[bs];
       int4* cbuf = cur ? cache1 : cache0;
       int4* nbuf = nxt ? cache1 : cache0;
@@ -1213,12 +1250,13 @@ __global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, 
                                                        const uint8_t* __restrict__ slot_in,
                                                        const uint8_t* __restrict__ slot_out,
                                                        const int32_t* __restrict__ rows, int32_t* counts,
-                                                       const char* __restrict__ fresh, int compact, int fresh_rows) {
+                                                       const char* __restrict__ fresh, int compact, int fresh_rows,
+                                                       int32_t* __restrict__ status) {
   extern __shared__ __align__(128) unsigned char smem[];  // [NL][SL][row_bytes] | offs[batch + 1]
   __shared__ __align__(8) uint64_t bar[NL * SL];
   const int lane = threadIdx.x;
   int* offs = reinterpret_cast<int*>(smem + (size_t)NL * SL * row_bytes);
-  if (lane < NL * SL) tma::bar_init(&bar[lane], 1);
+  for (int i = lane; i < NL * SL; i += 32) tma::bar_init(&bar[i], 1);
   // exclusive scan of counts (lane-contiguous segments)
   const int per = (batch + 31) / 32, q0 = lane * per, q1 = min(batch, q0 + per);
   int sum = 0;
@@ -1246,7 +1284,9 @@ __global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, 
   // one row per atomic
   constexpr int G = FC_SPLICE_CLAIM;
   int claim = 0, left = 0;
-  for (int it = 0;; ++it) {
+  // `it` counts issued rows only, so every slot's mbarrier phase advances
+  // once per use even when a malformed row is skipped
+  for (int it = 0;;) {
     if (left == 0) {
       claim = atomicAdd(work, G);
       left = G;
@@ -1268,6 +1308,10 @@ __global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, 
       const size_t base = (size_t)bs * n_tokens;
       const int p = rows[base + k];
       const int s = src_map[base + p];
+      if (!splice_src_ok(s, n_tokens, true, compact, fresh_rows)) {
+        flag_bounds(status);
+        continue;
+      }
       const int cur = slot_in[bs], nxt = slot_out[bs];
       const char* cbuf = cur ? cache1 : cache0;
       char* nbuf = nxt ? cache1 : cache0;
@@ -1293,6 +1337,7 @@ __global__ void __launch_bounds__(32) k_splice_ip_bulk(int batch, int n_tokens, 
     pdst = dst;
     pslot = sl;
     pphase = (it / SL) & 1;
+    ++it;
   }
   tma::bulk_wait0();
 }

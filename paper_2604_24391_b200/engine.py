@@ -57,6 +57,7 @@ class SelectResult:
     reuse_mask: torch.Tensor     # [B, N] uint8
     refresh_mask: torch.Tensor   # [B, N] uint8
     energy: torch.Tensor         # [B, N] float64
+    counters: torch.Tensor = None  # optional int64 [4]: frames, reused tokens, flushes, cold (accumulated)
 
     def host_results(self):
         return self.results.cpu().numpy().view(nat.RESULT_DTYPE).reshape(-1)
@@ -143,9 +144,12 @@ class FreqCacheEngine:
         cols, rows_inv, select) — synchronises; benchmarking only."""
         self._check_frames(frames)
         out = self.out if out is None else out
+        if out.counters is not None and (out.counters.dtype != torch.int64 or out.counters.numel() < 4
+                                         or out.counters.device != self.device):
+            raise ValueError("counters must be an int64 tensor of >= 4 elements on the engine's device")
         so = nat.SelectOut(out.results.data_ptr(), out.reuse_idx.data_ptr(), out.recompute_idx.data_ptr(),
                            out.src_map.data_ptr(), out.reuse_mask.data_ptr(), out.refresh_mask.data_ptr(),
-                           out.energy.data_ptr())
+                           out.energy.data_ptr(), out.counters.data_ptr() if out.counters is not None else None)
         conf = make_config(cfg, refresh_shift)
         with torch.cuda.device(self.device):
             if profile is None:
@@ -233,14 +237,34 @@ def row_cosines(a, b, out=None):
     return out
 
 
-def splice(src_map, cache, cache_ages, fresh, out, out_ages, compact=False):
+def _status_word(device):
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def check_status(status, what="splice"):
+    """Raise the reference's AssertionError (fusion.py:488-490) if a splice
+    kernel flagged an out-of-bounds source in ``status`` (synchronises)."""
+    code = int(status.reshape(-1)[0].item())
+    if code != nat.FC_OK:
+        nat.check(code, what)
+
+
+def splice(src_map, cache, cache_ages, fresh, out, out_ages, compact=False, status=None):
     """Token splice on device (fusion.py:462-512), any element type.
 
     src_map [B, N] int32; cache/fresh/out [B, N, D] (fresh may be [B, K, D]
     front-packed when ``compact``); ages int64 [B, N].  ``cache`` may be None
     when no entry of src_map is >= 0 (cold start / flush).
+
+    Every row's source is bounds-checked on the device (fusion.py:488-490).
+    With ``status=None`` the call allocates a status word and checks it after
+    the splice (one synchronisation), raising ``AssertionError`` on a bad
+    source; pass a zeroed device int32 tensor to keep the call asynchronous
+    and check it later with :func:`check_status`.
     """
     lib = nat.lib()
+    if src_map.dtype != torch.int32 or src_map.dim() != 2:
+        raise ValueError("src_map must be an int32 [B, N] tensor")
     B, N = src_map.shape
     row_bytes = out.shape[-1] * out.element_size()
     for t in (src_map, fresh, out, out_ages) + ((cache, cache_ages) if cache is not None else ()):
@@ -252,17 +276,21 @@ def splice(src_map, cache, cache_ages, fresh, out, out_ages, compact=False):
         raise ValueError("fresh rows must match out's dtype and row width")
     if fresh.dim() != 3 or fresh.shape[0] != B or (not compact and fresh.shape[1] != N):
         raise ValueError("fresh must be [B, N, D] (dense) or [B, K, D] (compact)")
+    st = _status_word(out.device) if status is None else status
     rc = lib.fc_splice(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(cache),
                        _ptr(cache_ages), _ptr(fresh),
                        nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE, int(fresh.shape[1]),
-                       _ptr(out), _ptr(out_ages), _stream(out.device))
+                       _ptr(out), _ptr(out_ages), _ptr(st), _stream(out.device))
     nat.check(rc, "fc_splice")
+    if status is None:
+        check_status(st, "fc_splice")
     return out, out_ages
 
 
-def splice_packed(src_map, cache, cache_ages, fresh_values, fresh_offsets, out, out_ages):
+def splice_packed(src_map, cache, cache_ages, fresh_values, fresh_offsets, out, out_ages, status=None):
     """Splice with ragged fresh rows: stream b's k-th recomputed token is
-    ``fresh_values[fresh_offsets[b] + k]`` ([total, D]; offsets int64 [B])."""
+    ``fresh_values[fresh_offsets[b] + k]`` ([total, D]; offsets int64 [B]).
+    ``status`` as in :func:`splice`."""
     lib = nat.lib()
     B, N = src_map.shape
     row_bytes = out.shape[-1] * out.element_size()
@@ -275,10 +303,13 @@ def splice_packed(src_map, cache, cache_ages, fresh_values, fresh_offsets, out, 
             raise ValueError("splice operands must be contiguous CUDA tensors")
     if cache is not None and (cache.dtype != out.dtype or cache.shape != out.shape):
         raise ValueError("cache and out must share dtype and shape")
+    st = _status_word(out.device) if status is None else status
     rc = lib.fc_splice_packed(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(cache), _ptr(cache_ages),
-                              _ptr(fresh_values), _ptr(fresh_offsets), _ptr(out), _ptr(out_ages),
+                              _ptr(fresh_values), _ptr(fresh_offsets), _ptr(out), _ptr(out_ages), _ptr(st),
                               _stream(out.device))
     nat.check(rc, "fc_splice_packed")
+    if status is None:
+        check_status(st, "fc_splice_packed")
     return out, out_ages
 
 
@@ -287,6 +318,9 @@ class SpliceState:
 
     ``cache`` [2, B, N, D] and ``ages`` [2, B, N]; ``slot[b]`` names the
     buffer that holds stream b's current cache (``current()`` gathers views).
+    Steps stay asynchronous: a malformed ``src_map`` row is skipped on the
+    device and recorded in ``status``; :meth:`check` raises the reference's
+    ``AssertionError`` (fusion.py:488-490) for it.
     """
 
     def __init__(self, cache, ages):
@@ -298,6 +332,7 @@ class SpliceState:
         self.k = 0
         nb = nat.lib().fc_splice_inplace_scratch_bytes(int(B), int(cache.shape[2]))
         self.scratch = torch.empty(nb, dtype=torch.uint8, device=cache.device)
+        self.status = _status_word(cache.device)
 
     @property
     def slot(self):
@@ -305,25 +340,74 @@ class SpliceState:
 
     def step(self, src_map, fresh, compact=False):
         lib = nat.lib()
+        dev = self.cache.device
+        if (src_map.dtype != torch.int32 or tuple(src_map.shape) != tuple(self.cache.shape[1:3])
+                or not src_map.is_contiguous() or src_map.device != dev):
+            raise ValueError(f"src_map must be a contiguous int32 {tuple(self.cache.shape[1:3])} tensor "
+                             "on the cache's device")
         B, N = src_map.shape
         row_bytes = self.cache.shape[-1] * self.cache.element_size()
         if fresh.dtype != self.cache.dtype or fresh.shape[-1] != self.cache.shape[-1] or fresh.shape[0] != B:
             raise ValueError("fresh must be [B, *, D] with the cache dtype")
+        if fresh.dim() != 3 or not fresh.is_contiguous() or fresh.device != dev:
+            raise ValueError("fresh must be a contiguous [B, *, D] tensor on the cache's device")
+        if not compact and fresh.shape[1] != N:
+            raise ValueError("dense fresh must be [B, N, D]")
         sin, sout = self.slots[self.k], self.slots[1 - self.k]
         rc = lib.fc_splice_inplace(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(self.cache[0]),
                                    _ptr(self.cache[1]), _ptr(self.ages[0]), _ptr(self.ages[1]), _ptr(sin),
                                    _ptr(sout), _ptr(fresh),
                                    nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE, int(fresh.shape[1]),
-                                   _ptr(self.scratch), _stream(self.cache.device))
+                                   _ptr(self.scratch), _ptr(self.status), _stream(self.cache.device))
         nat.check(rc, "fc_splice_inplace")
         self.k = 1 - self.k
         return self.slot
+
+    def check(self):
+        """Raise AssertionError if any step so far met an out-of-bounds
+        source (synchronises); clears the status word."""
+        try:
+            check_status(self.status, "fc_splice_inplace")
+        finally:
+            self.status.zero_()
 
     def current(self):
         """[B, N, D] tokens and [B, N] ages of every stream's current cache."""
         idx = self.slot.long()
         b = torch.arange(idx.numel(), device=idx.device)
         return self.cache[idx, b], self.ages[idx, b]
+
+
+class StepGraph:
+    """One captured step: everything ``fn()`` launches on the current CUDA
+    stream (and on streams forked from it through events) is recorded once
+    and replayed with a single graph launch (``fc_graph_*``).  ``fn`` must
+    not allocate device memory (all buffers exist before capture)."""
+
+    def __init__(self, fn, device=None):
+        self.lib = nat.lib()
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        st = _stream(self.device)
+        nat.check(self.lib.fc_graph_capture_begin(st), "fc_graph_capture_begin")
+        try:
+            fn()
+        finally:
+            ex = C.c_void_p()
+            rc = self.lib.fc_graph_capture_end(st, C.byref(ex))
+        nat.check(rc, "fc_graph_capture_end")
+        self._exec = ex
+
+    def replay(self):
+        nat.check(self.lib.fc_graph_launch(self._exec, _stream(self.device)), "fc_graph_launch")
+
+    def __del__(self):
+        ex = getattr(self, "_exec", None)
+        if ex is not None and ex.value:
+            try:
+                self.lib.fc_graph_destroy(ex)
+            except Exception:
+                pass
+            self._exec = None
 
 
 def splice_map(rows, cols, reuse_idx, di_patches, dj_patches, src_map=None, flag=None):

@@ -24,16 +24,49 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
 
 
 def test_reference_arm_nonzero_rank_exits_quietly():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "0", "--cpu-streams", "2", "--size", "224"],
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0", "--cpu-streams", "2", "--size", "224"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_world_size_mismatch_is_refused():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="4", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 2 and "refusing" in r.stderr
+
+
+@pytest.mark.parametrize("gpus,weak", [(8, False), (2, False), (4, True)])
+def test_gpus_flag_launches_ranks(gpus, weak):
+    """``bench.py --gpus N`` without torchrun re-launches itself with N ranks
+    (the launch path the driver's scaling run uses), here over gloo with
+    FC_BENCH_PLUMBING=1: config 5 read literally shards 512 streams into
+    512 / N contiguous blocks; --weak keeps 512 per rank; the max-over-ranks
+    time and the counter all-reduce reach rank 0, which alone prints."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["FC_BENCH_PLUMBING"] = "1"
+    args = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus), "--steps", "3"]
+    if weak:
+        args.append("--weak")
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == gpus and d["ms_max"] == float(gpus)          # rank r reports 1 + r ms
+    total = 512 * gpus if weak else 512
+    assert d["streams_total"] == total and sum(d["streams_per_rank"]) == total
+    assert d["streams_per_rank"] == [total // gpus] * gpus
+    assert [s[0] for s in d["spans"]] == [r * total // gpus for r in range(gpus)]
+    assert d["frames"] == total * 3
+    assert d["scaling"] == ("weak" if weak else "strong")
 
 
 @pytest.mark.gpu
@@ -59,5 +92,5 @@ def test_gpu_arm_json_line():
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] == 16 * 448 * 448 * 3 * 4 and e["d2h_bytes_per_step"] > 0 and e["value"] > 0
     assert d["e2e_u8"]["h2d_bytes_per_step"] == 16 * 448 * 448 * 3
-    assert d["gpu_launches"] > 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["gpu_launches"] > 0 and d["cpu_baseline"]["kind"] in ("port", "reference")
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}

@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol(lib):
     assert decl == set(_native.EXPORTS)
     for name in decl:
         assert hasattr(lib, name), name
-    assert lib.fc_abi_version() == 1
+    assert lib.fc_abi_version() == 2
     assert lib.fc_strerror(5).decode() == "normalized entropy must lie in [0, 1]"
 
 
@@ -85,14 +85,14 @@ def test_splice_rejects_bad_arguments_without_device(lib):
     from paper_2604_24391_b200 import _native
     p = ctypes.c_void_p(4096)   # never dereferenced: every call below is refused first
     big = 1 << 16
-    assert lib.fc_splice(big, big, 32, p, p, p, p, 0, 0, p, p, None) == _native.FC_EINVAL
-    assert lib.fc_splice(1, 4, 32, p, p, p, p, 7, 0, p, p, None) == _native.FC_EINVAL
-    assert lib.fc_splice(1, 4, 32, p, p, p, p, 1, 0, p, p, None) == _native.FC_EINVAL   # compact, no rows
-    assert lib.fc_splice_inplace(big, big, 32, p, p, p, p, p, p, p, p, 0, 0, p, None) == _native.FC_EINVAL
-    assert lib.fc_splice_inplace(1, 4, 24, p, p, p, p, p, p, p, p, 0, 0, p, None) == _native.FC_EINVAL
-    assert lib.fc_splice_inplace(1, 4, 32, p, p, p, p, p, p, p, p, 1, 0, p, None) == _native.FC_EINVAL
+    assert lib.fc_splice(big, big, 32, p, p, p, p, 0, 0, p, p, None, None) == _native.FC_EINVAL
+    assert lib.fc_splice(1, 4, 32, p, p, p, p, 7, 0, p, p, None, None) == _native.FC_EINVAL
+    assert lib.fc_splice(1, 4, 32, p, p, p, p, 1, 0, p, p, None, None) == _native.FC_EINVAL   # compact, no rows
+    assert lib.fc_splice_inplace(big, big, 32, p, p, p, p, p, p, p, p, 0, 0, p, None, None) == _native.FC_EINVAL
+    assert lib.fc_splice_inplace(1, 4, 24, p, p, p, p, p, p, p, p, 0, 0, p, None, None) == _native.FC_EINVAL
+    assert lib.fc_splice_inplace(1, 4, 32, p, p, p, p, p, p, p, p, 1, 0, p, None, None) == _native.FC_EINVAL
     assert lib.fc_splice_inplace(1, 4, 32, p, ctypes.c_void_p(4100), p, p, p, p, p, p, 0, 0, p,
-                                 None) == _native.FC_EINVAL   # misaligned cache
+                                 None, None) == _native.FC_EINVAL   # misaligned cache
 
 
 def test_product_path_fails_loudly_without_gpu():
@@ -203,3 +203,16 @@ def test_two_rank_gloo_metric_gather():
         assert c["reused_tokens"] == 256 * 100 + 256 * 101
         assert c["flushes"] == 6
         assert t == 2.0
+
+
+def test_psi_status_maps_to_reference_error():
+    """FC_EPSI from the select kernel surfaces as budget.py:69-70's ValueError
+    (host-side mapping, no device needed)."""
+    import numpy as np
+    from paper_2604_24391_b200 import _native as nat
+    from paper_2604_24391_b200.api import _raise_status
+    rec = np.zeros(1, dtype=nat.RESULT_DTYPE)[0]
+    rec["status"] = nat.FC_EPSI
+    rec["entropy_norm"] = 1.0000000000000002
+    with pytest.raises(ValueError, match=r"normalized entropy must lie in \[0, 1\], got 1.0000000000000002"):
+        _raise_status(rec)

@@ -63,13 +63,19 @@ def test_generator_is_frozen_and_c1_matches_reference():
 
 
 def test_c2_shift_rule_matches_reference_adapter():
+    """The oracle reproduces every one of golden_c2's 26 reference decisions
+    (2 streams x 13 steps at 448x448, config-2 shift rule) exactly."""
     from paper_2604_24391_b200.synth import stream_frames
     gold = json.loads((GOLD / "golden_c2.json").read_text())
     cfg = _ocfg({"patch_size": C2["patch"], "refresh_shift": C2["refresh_shift"]})
-    fr = stream_frames(C2["seed"], 0, 4, C2["size"], C2["size"])
-    assert [fhash(f) for f in fr] == gold["streams"][0]["frames"][:4]
-    for t in range(1, 4):
-        _same(O.decide(fr[t - 1], fr[t], cfg, step=t), gold["streams"][0]["decisions"][t - 1])
+    n = 0
+    for s, rec in enumerate(gold["streams"]):
+        fr = stream_frames(C2["seed"], s, C2["steps"], C2["size"], C2["size"])
+        assert [fhash(f) for f in fr] == rec["frames"]
+        for t in range(1, C2["steps"]):
+            _same(O.decide(fr[t - 1], fr[t], cfg, step=t), rec["decisions"][t - 1])
+            n += 1
+    assert n == 26
 
 
 def test_splice_matches_reference_step():
