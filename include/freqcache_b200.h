@@ -135,6 +135,7 @@ void fc_plan_destroy(fc_plan* plan);
 int64_t fc_plan_state_bytes(const fc_plan* plan);     /* per-stream state x B */
 int64_t fc_plan_workspace_bytes(const fc_plan* plan); /* scratch             */
 int  fc_plan_tokens(const fc_plan* plan);             /* N = rows*cols        */
+int  fc_plan_launches(const fc_plan* plan);           /* kernels per fc_select */
 
 /* Mark streams [first, first+count) cold. */
 int  fc_state_reset(const fc_plan* plan, void* state, int32_t first,
@@ -148,9 +149,28 @@ int  fc_select(const fc_plan* plan, const fc_config* cfg, const void* frames,
                void* state, void* workspace, const fc_select_out* out,
                void* cuda_stream);
 
-/* fc_select with a CUDA event after every launch; synchronises the stream
- * and returns per-kernel-kind device time in kernel_ms[4] (rows_fwd, cols,
- * rows_inv, select), summed over stream chunks.  For benchmarking. */
+/* Split-phase fc_select for software-pipelined streams of steps.  The
+ * front of a step (luma + block-DCT energies + row FFTs, K_A, and the
+ * energy statistics / refresh mask / token order, K_D1) depends on the
+ * frames only; the back (column FFTs, cross-power, inverse, argmax and the
+ * decision, K_B + K_C + K_D) on the front of the same step and on the back
+ * of the previous step (the spectrum state).  The front -> back
+ * intermediates live in workspace slot `slot` (0 / 1), so the front of step
+ * t + 1 (slot (t + 1) & 1) may run concurrently with the back of step t
+ * (slot t & 1) on different streams.  front(slot) then back(slot) on one
+ * stream equals fc_select.  Use the same `out` for a step's front and back
+ * (the front writes out->energy), and a different one for the next step. */
+int  fc_select_front(const fc_plan* plan, const fc_config* cfg, const void* frames,
+                     void* workspace, const fc_select_out* out, int32_t slot,
+                     void* cuda_stream);
+int  fc_select_back(const fc_plan* plan, const fc_config* cfg, void* state,
+                    void* workspace, const fc_select_out* out, int32_t slot,
+                    void* cuda_stream);
+
+/* fc_select with a CUDA event after every launch, all launches serial on
+ * the caller's stream; synchronises and returns per-kernel-kind device time
+ * in kernel_ms[4] (rows_fwd, cols, rows_inv, select = K_D1 + K_D), summed
+ * over stream chunks.  For benchmarking. */
 int  fc_select_profile(const fc_plan* plan, const fc_config* cfg, const void* frames,
                        void* state, void* workspace, const fc_select_out* out,
                        float* kernel_ms, void* cuda_stream);

@@ -41,8 +41,8 @@ FC_FRESH_COMPACT = 1
 
 EXPORTS = (
     "fc_abi_version", "fc_strerror", "fc_plan_create", "fc_plan_destroy",
-    "fc_plan_state_bytes", "fc_plan_workspace_bytes", "fc_plan_tokens",
-    "fc_state_reset", "fc_select", "fc_select_profile", "fc_patch_energy", "fc_splice",
+    "fc_plan_state_bytes", "fc_plan_workspace_bytes", "fc_plan_tokens", "fc_plan_launches",
+    "fc_state_reset", "fc_select", "fc_select_front", "fc_select_back", "fc_select_profile", "fc_patch_energy", "fc_splice",
     "fc_splice_map", "fc_stage_workspace_bytes", "fc_amp_cosine", "fc_spectral_sums",
     "fc_refresh_mask", "fc_topk_ascending", "fc_render_masks", "fc_splice_packed",
     "fc_splice_inplace", "fc_splice_inplace_scratch_bytes", "fc_compare_cosines", "fc_row_cosines",
@@ -108,8 +108,11 @@ def load(path=None):
         "fc_plan_state_bytes": (i64, [vp]),
         "fc_plan_workspace_bytes": (i64, [vp]),
         "fc_plan_tokens": (C.c_int, [vp]),
+        "fc_plan_launches": (C.c_int, [vp]),
         "fc_state_reset": (C.c_int, [vp, vp, i32, i32, vp]),
         "fc_select": (C.c_int, [vp, C.POINTER(Config), vp, vp, vp, C.POINTER(SelectOut), vp]),
+        "fc_select_front": (C.c_int, [vp, C.POINTER(Config), vp, vp, C.POINTER(SelectOut), i32, vp]),
+        "fc_select_back": (C.c_int, [vp, C.POINTER(Config), vp, vp, C.POINTER(SelectOut), i32, vp]),
         "fc_select_profile": (C.c_int, [vp, C.POINTER(Config), vp, vp, vp, C.POINTER(SelectOut),
                                         C.POINTER(C.c_float), vp]),
         "fc_patch_energy": (C.c_int, [vp, vp, vp, vp, vp]),

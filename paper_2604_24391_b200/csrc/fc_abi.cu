@@ -28,6 +28,7 @@ namespace {
 constexpr int kChunkDefault = 512;  // streams per A/B/C launch group on the fast path
 constexpr int kLanesDefault = 1;   // concurrent chunk lanes (internal CUDA streams)
 constexpr int kMaxLanes = 8;
+constexpr int kSmallBatch = 128;   // at or below: two half-batch chunks on two lanes
 
 int env_int(const char* name, int dflt, int lo, int hi) {
   const char* v = std::getenv(name);
@@ -44,10 +45,14 @@ struct fc_plan {
   bool fast = false;
   int chunk = 0;
   int lanes = 1;                       // fast path: chunk groups in flight
-  cudaStream_t lane[kMaxLanes] = {};   // internal non-blocking streams
-  cudaEvent_t fork = nullptr;
-  cudaEvent_t join[kMaxLanes] = {};
-  size_t lane_stride = 0;              // workspace bytes per lane (T1 + T2)
+  // internal non-blocking lane streams and fork / join events, one set per
+  // part (whole select, split-phase front, split-phase back)
+  cudaStream_t lanes3[3][kMaxLanes] = {};
+  cudaEvent_t fork3[3] = {};
+  cudaEvent_t join3[3][kMaxLanes] = {};
+  size_t lane_stride = 0;              // workspace bytes per lane (2 T1 slots + T2)
+  // split-phase select: per-slot strides of the front -> back intermediates
+  size_t slot_T = 0, slot_stripes = 0, slot_order = 0, slot_freshm = 0, slot_estats = 0;
   void* fnB = nullptr;                 // K_B / K_C variants (occupancy x twiddle mode)
   bool t2_tma = false;                 // K_B stores T2 with a TMA tensor store
   bool t1_tma = false;                 // K_A stores T1 with a TMA tensor store
@@ -59,6 +64,10 @@ struct fc_plan {
   float2* d_tw64 = nullptr;
   size_t smemA = 0, smemB = 0, smemC = 0, smemD = 0;
   size_t off_T = 0, off_T2 = 0, off_stripes = 0, off_stats = 0, off_peaks = 0, off_energy = 0, ws_bytes = 0;
+  size_t off_order = 0, off_freshm = 0, off_estats = 0;
+  size_t smemR = 0;                    // K_D1 (k_rank) dynamic shared memory
+  cudaStream_t aux = nullptr;          // K_D1 branch beside K_B / K_C
+  cudaEvent_t ev_a = nullptr, ev_aux = nullptr;
   size_t state_hdr_bytes = 0, state_bytes = 0;
   int kw = 0, kh = 0;  // fixed-size generic FFT variants (0 = runtime plan)
 };
@@ -121,7 +130,10 @@ void* sel_fast_rows_fwd(int fmt, bool tm) { return tm ? sel_fast_rows_fwd_t<true
 using FastRowsFwd = void (*)(KParams, Dct14, const void*, int, int, CUtensorMap);
 
 int set_smem(void* fn, size_t bytes) {
-  if (bytes > 48 * 1024) {
+  // the 48 KB default covers static + dynamic shared memory: opt in above it
+  cudaFuncAttributes fa;
+  const size_t stat = cudaFuncGetAttributes(&fa, fn) == cudaSuccess ? fa.sharedSizeBytes : 0;
+  if (bytes + stat > 48 * 1024) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
       return FC_ECUDA;
   }
@@ -135,15 +147,18 @@ int launch_check() {
   return e == cudaSuccess ? FC_OK : FC_ECUDA;
 }
 
-KParams bind(const fc_plan* pl, void* state, void* ws, double* energy) {
+KParams bind(const fc_plan* pl, void* state, void* ws, double* energy, int slot = 0) {
   KParams kp = pl->kp;
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
-  kp.T = reinterpret_cast<float2*>(w + pl->off_T);
+  kp.T = reinterpret_cast<float2*>(w + pl->off_T + slot * pl->slot_T);
   kp.T2 = pl->fast ? reinterpret_cast<float2*>(w + pl->off_T2) : nullptr;
-  kp.stripes = reinterpret_cast<StripeStat*>(w + pl->off_stripes);
+  kp.stripes = reinterpret_cast<StripeStat*>(w + pl->off_stripes + slot * pl->slot_stripes);
   kp.stats = reinterpret_cast<double*>(w + pl->off_stats);
   kp.peaks = reinterpret_cast<PeakPart*>(w + pl->off_peaks);
   kp.energy = energy ? energy : reinterpret_cast<double*>(w + pl->off_energy);
+  kp.order = reinterpret_cast<int16_t*>(w + pl->off_order + slot * pl->slot_order);
+  kp.freshm = w + pl->off_freshm + slot * pl->slot_freshm;
+  kp.estats = reinterpret_cast<double*>(w + pl->off_estats + slot * pl->slot_estats);
   if (state) {
     uint8_t* s = reinterpret_cast<uint8_t*>(state);
     kp.hdr = reinterpret_cast<StreamHdr*>(s);
@@ -220,12 +235,45 @@ bool encode_t1_map(CUtensorMap* map, void* t1, int chunk) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// K_D1 for streams [b0, b0 + nb) once their energies exist (after K_A on
+// `after`).  fc_select forks it onto the plan's aux stream so it runs beside
+// K_B / K_C; the split-phase front (and profiling) launch it in order on
+// `after` itself (`fork` false).
+void launch_rank(const fc_plan* pl, const fc_config& cfg, const KParams& kp, int b0, int nb, cudaStream_t after,
+                 bool fork, Recorder* rec) {
+  cudaStream_t rs = after;
+  if (fork) {
+    cudaEventRecord(pl->ev_a, after);
+    cudaStreamWaitEvent(pl->aux, pl->ev_a, 0);
+    rs = pl->aux;
+  }
+  if (nb <= kSmallBatch) k_rank<512><<<nb, 512, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
+  else k_rank<FC_SEL_THREADS><<<nb, FC_SEL_THREADS, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
+  if (rec) rec->mark(after, 3);
+}
+
+// Which kernels a call launches: the whole select, or one half of the
+// split-phase select (front: K_A + K_D1 of a step; back: K_B + K_C + K_D).
+enum Part { kAll = 0, kFront = 1, kBack = 2 };
+
+// Internal lane streams and fork / join events of one part: the front of
+// step t + 1 and the back of step t run concurrently, so they never share a
+// stream (which would serialise them) or an event.
+struct LaneSet {
+  const cudaStream_t* lane;
+  cudaEvent_t fork;
+  const cudaEvent_t* join;
+};
+
 // Returns FC_OK, or FC_ECUDA (nothing launched) when a tensor map cannot be
 // encoded for this call's workspace.
 int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, const KParams& kp,
-                  const fc_select_out& out, cudaStream_t st, Recorder* rec) {
+                  const fc_select_out& out, cudaStream_t st, Recorder* rec, Part part = kAll) {
   const int B = pl->g.batch;
+  const bool front = part != kBack, back = part != kFront;
   if (pl->fast) {
+    const int ls_i = part == kAll ? 0 : part == kFront ? 1 : 2;
+    const LaneSet set = {pl->lanes3[ls_i], pl->fork3[ls_i], pl->join3[ls_i]};
     // tensor maps of every lane's T1 / T2 first, so a failure launches nothing
     CUtensorMap tm1[kMaxLanes], tm2[kMaxLanes];
     std::memset(tm1, 0, sizeof(tm1));
@@ -234,8 +282,8 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
     for (int l = 0; l < nmaps; ++l) {
       uint8_t* t1 = reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride;
       uint8_t* t2 = reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride;
-      if (pl->t1_tma && !encode_t1_map(&tm1[l], t1, pl->chunk)) return FC_ECUDA;
-      if (pl->t2_tma && !encode_t2_map(&tm2[l], t2, pl->chunk)) return FC_ECUDA;
+      if (front && pl->t1_tma && !encode_t1_map(&tm1[l], t1, pl->chunk)) return FC_ECUDA;
+      if (back && pl->t2_tma && !encode_t2_map(&tm2[l], t2, pl->chunk)) return FC_ECUDA;
     }
     // Chunks of `chunk` streams run A -> B -> C on `lanes` internal streams
     // (each lane owns its T1/T2 slice) so one chunk's tail overlaps the next
@@ -244,43 +292,58 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
     auto fa = (FastRowsFwd)sel_fast_rows_fwd(pl->g.format, pl->t1_tma);
     const int nl = rec ? 1 : pl->lanes;
     if (!rec) {
-      cudaEventRecord(pl->fork, st);
-      for (int l = 0; l < nl; ++l) cudaStreamWaitEvent(pl->lane[l], pl->fork, 0);
+      cudaEventRecord(set.fork, st);
+      for (int l = 0; l < nl; ++l) cudaStreamWaitEvent(set.lane[l], set.fork, 0);
     }
     int c = 0;
     for (int b0 = 0; b0 < B; b0 += pl->chunk, ++c) {
       const int nb = B - b0 < pl->chunk ? B - b0 : pl->chunk;
       const int l = c % nl;
-      const cudaStream_t ls = rec ? st : pl->lane[l];
+      const cudaStream_t ls = rec ? st : set.lane[l];
       KParams kl = kp;
       kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride);
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
-      fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1, tm1[l]);
-      if (rec) rec->mark(st, 0);
-      auto fb = (void (*)(KParams, int, CUtensorMap))pl->fnB;
-      fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm2[l]);
-      if (rec) rec->mark(st, 1);
-      auto fc = (void (*)(KParams, int))pl->fnC;
-      fc<<<dim3(kNRG448, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
-      if (rec) rec->mark(st, 2);
+      if (front) {
+        fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1, tm1[l]);
+        if (rec) rec->mark(st, 0);
+        launch_rank(pl, cfg, kp, b0, nb, ls, part == kAll && !rec, rec);
+      }
+      if (back) {
+        auto fb = (void (*)(KParams, int, CUtensorMap))pl->fnB;
+        fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm2[l]);
+        if (rec) rec->mark(st, 1);
+        auto fc = (void (*)(KParams, int))pl->fnC;
+        fc<<<dim3(kNRG448, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
+        if (rec) rec->mark(st, 2);
+      }
     }
     if (!rec) {
       for (int l = 0; l < nl; ++l) {
-        cudaEventRecord(pl->join[l], pl->lane[l]);
-        cudaStreamWaitEvent(st, pl->join[l], 0);
+        cudaEventRecord(set.join[l], set.lane[l]);
+        cudaStreamWaitEvent(st, set.join[l], 0);
       }
     }
   } else {
     const dim3 blk(FC_THREADS);
-    auto fa = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
-    fa<<<dim3(kp.rows, B), blk, pl->smemA, st>>>(kp, frames, 1);
-    if (rec) rec->mark(st, 0);
-    auto fb = (void (*)(KParams))sel_cols(pl->kh);
-    fb<<<dim3(kp.NCB, B), blk, pl->smemB, st>>>(kp);
-    if (rec) rec->mark(st, 1);
-    auto fc = (void (*)(KParams))sel_rows_inv(pl->kw);
-    fc<<<dim3(kp.NRG, B), blk, pl->smemC, st>>>(kp);
-    if (rec) rec->mark(st, 2);
+    if (front) {
+      auto fa = (void (*)(KParams, const void*, int))sel_rows_fwd(pl->kw);
+      fa<<<dim3(kp.rows, B), blk, pl->smemA, st>>>(kp, frames, 1);
+      if (rec) rec->mark(st, 0);
+      launch_rank(pl, cfg, kp, 0, B, st, part == kAll && !rec, rec);
+    }
+    if (back) {
+      auto fb = (void (*)(KParams))sel_cols(pl->kh);
+      fb<<<dim3(kp.NCB, B), blk, pl->smemB, st>>>(kp);
+      if (rec) rec->mark(st, 1);
+      auto fc = (void (*)(KParams))sel_rows_inv(pl->kw);
+      fc<<<dim3(kp.NRG, B), blk, pl->smemC, st>>>(kp);
+      if (rec) rec->mark(st, 2);
+    }
+  }
+  if (!back) return FC_OK;
+  if (part == kAll && !rec) {  // K_D waits for the K_D1 branch
+    cudaEventRecord(pl->ev_aux, pl->aux);
+    cudaStreamWaitEvent(st, pl->ev_aux, 0);
   }
   // small batches leave SMs idle during the per-stream selection: give each
   // stream more threads there (FC_SEL_NT overrides)
@@ -346,13 +409,18 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
 
   int NP2 = 1;
   while (NP2 < N) NP2 <<= 1;
-  pl->smemD = (size_t)N * 8 + (size_t)NP2 * 8 + (size_t)NP2 * 4 + (size_t)N * 4 + (size_t)N * 2;
+  pl->smemD = (size_t)N * 4 * 2 + (size_t)N * 3;   // K_D: reuse list, ranks, fresh / reuse / candidate flags
+  pl->smemR = (size_t)NP2 * 8 + (size_t)NP2 * 4;    // K_D1: (E, index) sort keys
   size_t specElems, off = 0;
   if (pl->fast) {
-    const int want = env_int("FC_CHUNK", kChunkDefault, 1, 4096);
+    // small batches (e.g. 512 / N streams per GPU at N = 4, 8) run as two
+    // half-batch chunks on two lanes, so one chunk's kernel tails overlap the
+    // other's (64 streams: +7 % measured); larger batches as one chunk
+    const bool halves = B <= (size_t)kSmallBatch && B >= 2;
+    const int want = env_int("FC_CHUNK", halves ? (int)((B + 1) / 2) : kChunkDefault, 1, 4096);
     pl->chunk = (int)(B < (size_t)want ? B : (size_t)want);
     const int nchunks = (int)((B + pl->chunk - 1) / pl->chunk);
-    pl->lanes = env_int("FC_LANES", kLanesDefault, 1, kMaxLanes);
+    pl->lanes = env_int("FC_LANES", halves ? 2 : kLanesDefault, 1, kMaxLanes);
     if (pl->lanes > nchunks) pl->lanes = nchunks;
     pl->smemA = (size_t)kPxBytes448;
     pl->smemB = (size_t)kSmemB448;
@@ -362,9 +430,10 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     const size_t ch = pl->chunk;
     const size_t t1 = align_up(ch * 224 * 448 * sizeof(float2));
     const size_t t2 = align_up(ch * 448 * 224 * sizeof(float2));
-    pl->lane_stride = t1 + t2;
+    pl->lane_stride = 2 * t1 + t2;   // [T1 slot 0 | T1 slot 1 | T2] per lane
     pl->off_T = off;
-    pl->off_T2 = off + t1;
+    pl->off_T2 = off + 2 * t1;
+    pl->slot_T = t1;
     off += pl->lane_stride * pl->lanes;
     specElems = B * 224 * kStCol * 2;  // register-order state (float2 count)
   } else {
@@ -374,17 +443,30 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     pl->smemB = (size_t)2 * H * FC_CB * 8 + (size_t)H * 8;
     pl->smemC = (size_t)2 * maxpairC * W * 8 + (size_t)W * 8;
     specElems = B * kp.NCB * (size_t)H * FC_CB;
-    pl->off_T = off; off = align_up(off + specElems * sizeof(float2));
+    pl->off_T = off;
+    pl->slot_T = align_up(specElems * sizeof(float2));
+    off += 2 * pl->slot_T;
   }
   const size_t kMaxSmem = 227 * 1024;
   if (pl->smemA > kMaxSmem || pl->smemB > kMaxSmem || pl->smemC > kMaxSmem || pl->smemD > kMaxSmem) {
     delete pl;
     return FC_EUNSUPPORTED;
   }
-  pl->off_stripes = off; off = align_up(off + B * rows * sizeof(StripeStat));
+  pl->off_stripes = off;
+  pl->slot_stripes = align_up(B * rows * sizeof(StripeStat));
+  off += 2 * pl->slot_stripes;
   pl->off_stats = off; off = align_up(off + B * kp.NCB * 4 * sizeof(double));
   pl->off_peaks = off; off = align_up(off + B * kp.NRG * sizeof(PeakPart));
   pl->off_energy = off; off = align_up(off + B * N * sizeof(double));
+  pl->off_order = off;
+  pl->slot_order = align_up(B * N * sizeof(int16_t));
+  off += 2 * pl->slot_order;
+  pl->off_freshm = off;
+  pl->slot_freshm = align_up(B * N);
+  off += 2 * pl->slot_freshm;
+  pl->off_estats = off;
+  pl->slot_estats = align_up(B * 4 * sizeof(double));
+  off += 2 * pl->slot_estats;
   pl->ws_bytes = off;
   pl->state_hdr_bytes = align_up(B * sizeof(StreamHdr));
   pl->state_bytes = pl->state_hdr_bytes + align_up(specElems * sizeof(float2));
@@ -417,11 +499,16 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
   up((void**)&pl->d_dct, dct.data(), dct.size() * sizeof(double));
   up((void**)&pl->d_tw448, t448.data(), t448.size() * sizeof(float2));
   up((void**)&pl->d_tw64, t64.data(), t64.size() * sizeof(float2));
-  if (rc == FC_OK && pl->fast) {
-    if (cudaEventCreateWithFlags(&pl->fork, cudaEventDisableTiming) != cudaSuccess) rc = FC_ECUDA;
+  if (rc == FC_OK &&
+      (cudaStreamCreateWithFlags(&pl->aux, cudaStreamNonBlocking) != cudaSuccess ||
+       cudaEventCreateWithFlags(&pl->ev_a, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&pl->ev_aux, cudaEventDisableTiming) != cudaSuccess))
+    rc = FC_ECUDA;
+  for (int k = 0; k < 3 && rc == FC_OK && pl->fast; ++k) {
+    if (cudaEventCreateWithFlags(&pl->fork3[k], cudaEventDisableTiming) != cudaSuccess) rc = FC_ECUDA;
     for (int l = 0; l < pl->lanes && rc == FC_OK; ++l) {
-      if (cudaStreamCreateWithFlags(&pl->lane[l], cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&pl->join[l], cudaEventDisableTiming) != cudaSuccess)
+      if (cudaStreamCreateWithFlags(&pl->lanes3[k][l], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&pl->join3[k][l], cudaEventDisableTiming) != cudaSuccess)
         rc = FC_ECUDA;
     }
   }
@@ -460,6 +547,8 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     if (rc == FC_OK) rc = set_smem((void*)k_select<FC_SEL_THREADS>, pl->smemD);
     if (rc == FC_OK) rc = set_smem((void*)k_select<512>, pl->smemD);
     if (rc == FC_OK) rc = set_smem((void*)k_select<1024>, pl->smemD);
+    if (rc == FC_OK) rc = set_smem((void*)k_rank<FC_SEL_THREADS>, pl->smemR);
+    if (rc == FC_OK) rc = set_smem((void*)k_rank<512>, pl->smemR);
   }
   if (rc != FC_OK) {
     fc_plan_destroy(pl);
@@ -481,17 +570,27 @@ void fc_plan_destroy(fc_plan* pl) {
   if (pl->d_dct) cudaFree(pl->d_dct);
   if (pl->d_tw448) cudaFree(pl->d_tw448);
   if (pl->d_tw64) cudaFree(pl->d_tw64);
-  for (int l = 0; l < kMaxLanes; ++l) {
-    if (pl->lane[l]) cudaStreamDestroy(pl->lane[l]);
-    if (pl->join[l]) cudaEventDestroy(pl->join[l]);
+  for (int k = 0; k < 3; ++k) {
+    for (int l = 0; l < kMaxLanes; ++l) {
+      if (pl->lanes3[k][l]) cudaStreamDestroy(pl->lanes3[k][l]);
+      if (pl->join3[k][l]) cudaEventDestroy(pl->join3[k][l]);
+    }
+    if (pl->fork3[k]) cudaEventDestroy(pl->fork3[k]);
   }
-  if (pl->fork) cudaEventDestroy(pl->fork);
+  if (pl->aux) cudaStreamDestroy(pl->aux);
+  if (pl->ev_a) cudaEventDestroy(pl->ev_a);
+  if (pl->ev_aux) cudaEventDestroy(pl->ev_aux);
   delete pl;
 }
 
 int64_t fc_plan_state_bytes(const fc_plan* pl) { return pl ? (int64_t)pl->state_bytes : -1; }
 int64_t fc_plan_workspace_bytes(const fc_plan* pl) { return pl ? (int64_t)pl->ws_bytes : -1; }
 int fc_plan_tokens(const fc_plan* pl) { return pl ? pl->kp.N : -1; }
+int fc_plan_launches(const fc_plan* pl) {
+  if (!pl) return -1;
+  // fast: K_A, K_D1, K_B, K_C per chunk + K_D; generic: the five kernels once
+  return pl->fast ? 4 * ((pl->g.batch + pl->chunk - 1) / pl->chunk) + 1 : 5;
+}
 
 int fc_state_reset(const fc_plan* pl, void* state, int32_t first, int32_t count, void* stream) {
   if (!pl || !state || first < 0 || count < 0 || first + count > pl->g.batch) return FC_EINVAL;
@@ -516,6 +615,31 @@ int fc_select(const fc_plan* pl, const fc_config* cfg, const void* frames, void*
   return launch_check();
 }
 
+int fc_select_front(const fc_plan* pl, const fc_config* cfg, const void* frames, void* ws,
+                    const fc_select_out* out, int32_t slot, void* stream) {
+  if (!pl || !cfg || !frames || !ws || !out || (slot != 0 && slot != 1)) return FC_EINVAL;
+  if (((pl->fast ? reinterpret_cast<uintptr_t>(frames) : 0) | reinterpret_cast<uintptr_t>(ws)) & 15)
+    return FC_EINVAL;
+  const int rc = check_cfg(cfg);
+  if (rc != FC_OK) return rc;
+  const KParams kp = bind(pl, nullptr, ws, out->energy, slot);
+  const int lrc = launch_select(pl, *cfg, frames, kp, *out, as_stream(stream), nullptr, kFront);
+  if (lrc != FC_OK) return lrc;
+  return launch_check();
+}
+
+int fc_select_back(const fc_plan* pl, const fc_config* cfg, void* state, void* ws, const fc_select_out* out,
+                   int32_t slot, void* stream) {
+  if (!pl || !cfg || !state || !ws || !out || (slot != 0 && slot != 1)) return FC_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(state) | reinterpret_cast<uintptr_t>(ws)) & 15) return FC_EINVAL;
+  const int rc = check_cfg(cfg);
+  if (rc != FC_OK) return rc;
+  const KParams kp = bind(pl, state, ws, out->energy, slot);
+  const int lrc = launch_select(pl, *cfg, nullptr, kp, *out, as_stream(stream), nullptr, kBack);
+  if (lrc != FC_OK) return lrc;
+  return launch_check();
+}
+
 int fc_select_profile(const fc_plan* pl, const fc_config* cfg, const void* frames, void* state, void* ws,
                       const fc_select_out* out, float* kernel_ms, void* stream) {
   if (!pl || !cfg || !frames || !state || !ws || !out || !kernel_ms) return FC_EINVAL;
@@ -526,7 +650,7 @@ int fc_select_profile(const fc_plan* pl, const fc_config* cfg, const void* frame
   if (rc != FC_OK) return rc;
   const cudaStream_t st = as_stream(stream);
   const KParams kp = bind(pl, state, ws, out->energy);
-  const int cap = 3 * ((pl->g.batch + pl->chunk - 1) / pl->chunk) + 2;  // serial chunks
+  const int cap = 4 * ((pl->g.batch + pl->chunk - 1) / pl->chunk) + 3;  // serial chunks
   std::vector<cudaEvent_t> ev(cap);
   std::vector<int> kind(cap);
   for (auto& e : ev) cudaEventCreate(&e);

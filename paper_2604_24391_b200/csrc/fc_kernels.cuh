@@ -74,6 +74,9 @@ struct KParams {
   double* energy;  // [B][N]
   StreamHdr* hdr;
   float2* spec;
+  int16_t* order;   // [B][N] all tokens ascending (E, index) (K_D1 -> K_D)
+  uint8_t* freshm;  // [B][N] refresh mask (K_D1 -> K_D)
+  double* estats;   // [B][4] mean, std, threshold, refresh count (K_D1 -> K_D)
 };
 
 // --------------------------------------------------------------- helpers --
@@ -670,28 +673,107 @@ __device__ void bitonic_hybrid(double* ke, int* ki, int NP2) {
   }
 }
 
-// Decision for one stream (fusion.py:121-242 selection; 245-262 invariants
-// hold by construction).  Scalars in thread 0, per-token work spread.
+// K_D1: per-stream energy statistics, refresh mask and the ascending
+// (E, index) order of ALL tokens (edge_refresh.py:62-73, fusion.py:104-115).
+// It needs the energies only (K_A), so it runs on a side branch beside
+// K_B / K_C; K_D then takes the first K_final candidates of this order — a
+// stable filter of the sorted token list is exactly topk_ascending's lexsort
+// of the candidates — so no sort is left on the critical path.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_rank(KParams kp, double lam, int b0) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int b = b0 + blockIdx.x;
+  const int N = kp.N;
+  int NP2 = 1;
+  while (NP2 < N) NP2 <<= 1;
+  double* ke = reinterpret_cast<double*>(smem);  // NP2
+  int* ki = reinterpret_cast<int*>(ke + NP2);    // NP2
+  __shared__ double red[32 * 2];
+  __shared__ int redi[32];
+  const double* energy = kp.energy + (size_t)b * N;
+  for (int p = threadIdx.x; p < NP2; p += blockDim.x) {
+    ke[p] = p < N ? energy[p] : CUDART_INF;
+    ki[p] = p < N ? p : 0x7fffffff;
+  }
+  __syncthreads();
+
+  // Module II statistics: population mean / std.  Summation order fixed at
+  // FC_SEL_THREADS strided partials whatever the block size (the extra warps
+  // add exact zeros to the trees), so a stream's statistics do not depend on
+  // the batch size that picked the block size.
+  static_assert(NT % FC_SEL_THREADS == 0, "block size must be a multiple of the reduction width");
+  const bool red_lane = threadIdx.x < FC_SEL_THREADS;
+  double s1 = 0.0;
+  // shifted by E[0]: an all-equal energy map keeps an exact mean and std 0
+  const double e0 = ke[0];
+  if (red_lane)
+    for (int p = threadIdx.x; p < N; p += FC_SEL_THREADS) s1 += ke[p] - e0;
+  {
+    double v[1] = {s1};
+    block_sum_d<1>(v, red);
+    if (threadIdx.x == 0) red[63] = e0 + v[0] / (double)N;
+  }
+  __syncthreads();
+  const double mu = red[63];
+  double s2 = 0.0;
+  if (red_lane)
+    for (int p = threadIdx.x; p < N; p += FC_SEL_THREADS) { const double d = ke[p] - mu; s2 = fma(d, d, s2); }
+  {
+    double v[1] = {s2};
+    block_sum_d<1>(v, red);
+    if (threadIdx.x == 0) {
+      const double sd = sqrt(v[0] / (double)N);
+      red[62] = mu + lam * sd;
+      double* es = kp.estats + (size_t)b * 4;
+      es[0] = mu;
+      es[1] = sd;
+      es[2] = mu + lam * sd;
+    }
+  }
+  __syncthreads();
+  const double thr = red[62];
+  int nfresh = 0;
+  uint8_t* fm = kp.freshm + (size_t)b * N;
+  for (int p = threadIdx.x; p < N; p += blockDim.x) {
+    const int f = ke[p] > thr;   // strict (edge_refresh.py:72)
+    fm[p] = (uint8_t)f;
+    nfresh += f;
+  }
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int a = warp_sum(nfresh);
+    if (lane == 0) redi[wid] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int ta = 0;
+      for (int w = 0; w < nw; ++w) ta += redi[w];
+      kp.estats[(size_t)b * 4 + 3] = (double)ta;
+    }
+  }
+  // ascending (E, index) order of every token (fusion.py:104-115)
+  if (NP2 >= 64) bitonic_hybrid(ke, ki, NP2);
+  else bitonic_smem(ke, ki, NP2);
+  int16_t* ord = kp.order + (size_t)b * N;
+  for (int r = threadIdx.x; r < N; r += blockDim.x) ord[r] = (int16_t)ki[r];
+}
+
+// K_D: decision for one stream (fusion.py:121-242 selection; 245-262
+// invariants hold by construction).  Scalars in thread 0, per-token work
+// spread; the energy statistics, refresh mask and token order come from K_D1.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_select_out out) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int b = blockIdx.x;
   const int N = kp.N;
-  int NP2 = 1;
-  while (NP2 < N) NP2 <<= 1;
-  double* E = reinterpret_cast<double*>(smem);   // N
-  double* ke = E + N;                            // NP2
-  int* ki = reinterpret_cast<int*>(ke + NP2);    // NP2
-  int* rank = ki + NP2;                          // N
+  int* ki = reinterpret_cast<int*>(smem);                 // N: reuse list
+  int* rank = ki + N;                                     // N
   uint8_t* fresh = reinterpret_cast<uint8_t*>(rank + N);  // N
-  uint8_t* reuse = fresh + N;                              // N
+  uint8_t* reuse = fresh + N;                             // N
+  uint8_t* cand = reuse + N;                              // N
   __shared__ double red[32 * 2];
   __shared__ int redi[32];
   __shared__ fc_stream_result R;
   __shared__ int sh_flush, sh_dip, sh_djp, sh_kfinal, sh_err;
-
-  const double* energy = kp.energy + (size_t)b * N;
-  for (int p = threadIdx.x; p < N; p += blockDim.x) E[p] = energy[p];
 
   __shared__ double sh_sum[4], sh_ref;
   __shared__ int sh_bad, sh_vary, sh_pos;
@@ -740,6 +822,10 @@ __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_sel
       sh_sum[0] = a0; sh_sum[1] = a1; sh_sum[2] = a2; sh_sum[3] = a3;
       sh_pv = bk.v; sh_pv2 = v2; sh_pos = bk.pos;
     }
+  } else {
+    // the other warps stage K_D1's refresh mask meanwhile
+    const uint8_t* fm = kp.freshm + (size_t)b * N;
+    for (int p = threadIdx.x - 32; p < N; p += blockDim.x - 32) fresh[p] = fm[p];
   }
   __syncthreads();
 
@@ -803,6 +889,12 @@ __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_sel
       else flush = 0;
     }
     R.flushed = flush;
+    // Module II (edge_refresh.py:62-73), from K_D1
+    const double* es = kp.estats + (size_t)b * 4;
+    R.energy_mean = es[0];
+    R.energy_std = es[1];
+    R.energy_threshold = es[2];
+    R.n_refresh = (int)es[3];
     sh_flush = flush; sh_dip = dip; sh_djp = djp;
     sh_err = R.status != FC_OK;
     // state for the next step: this frame becomes "prev"
@@ -822,65 +914,26 @@ __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_sel
   }
   __syncthreads();
 
-  // Module II statistics (edge_refresh.py:62-73): population mean / std.
-  // Summation order fixed at FC_SEL_THREADS strided partials whatever the
-  // block size (the extra warps add exact zeros to the trees), so a stream's
-  // statistics do not depend on the batch size that picked the block size.
-  static_assert(NT % FC_SEL_THREADS == 0, "block size must be a multiple of the reduction width");
-  const bool red_lane = threadIdx.x < FC_SEL_THREADS;
-  double s1 = 0.0;
-  // shifted by E[0]: an all-equal energy map keeps an exact mean and std 0
-  const double e0 = E[0];
-  if (red_lane)
-    for (int p = threadIdx.x; p < N; p += FC_SEL_THREADS) s1 += E[p] - e0;
-  {
-    double v[1] = {s1};
-    block_sum_d<1>(v, red);
-    if (threadIdx.x == 0) red[63] = e0 + v[0] / (double)N;
-  }
-  __syncthreads();
-  const double mu = red[63];
-  double s2 = 0.0;
-  if (red_lane)
-    for (int p = threadIdx.x; p < N; p += FC_SEL_THREADS) { const double d = E[p] - mu; s2 = fma(d, d, s2); }
-  {
-    double v[1] = {s2};
-    block_sum_d<1>(v, red);
-    if (threadIdx.x == 0) {
-      const double sd = sqrt(v[0] / (double)N);
-      R.energy_mean = mu;
-      R.energy_std = sd;
-      R.energy_threshold = mu + cfg.edge_lambda * sd;
-    }
-  }
-  __syncthreads();
-  const double thr = R.energy_threshold;
   const int rows = kp.rows, cols = kp.cols;
   const int flush = sh_flush, dip = sh_dip, djp = sh_djp;
-  int nfresh = 0, ncand = 0;
+  int ncand = 0;
   for (int p = threadIdx.x; p < N; p += blockDim.x) {
-    const int f = E[p] > thr;
-    fresh[p] = (uint8_t)f;
-    nfresh += f;
     const int i = p / cols, j = p - (p / cols) * cols;
     const int si = i - dip, sj = j - djp;
     const int aligned = (si >= 0 && si < rows && sj >= 0 && sj < cols);
-    const int cand = !flush && aligned && !f;   // fusion.py:214
-    ncand += cand;
-    ke[p] = cand ? E[p] : CUDART_INF;
-    ki[p] = p;
+    const int c = !flush && aligned && !fresh[p];   // fusion.py:214
+    cand[p] = (uint8_t)c;
+    ncand += c;
     reuse[p] = 0;
   }
-  for (int p = N + threadIdx.x; p < NP2; p += blockDim.x) { ke[p] = CUDART_INF; ki[p] = 0x7fffffff; }
   {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int a = warp_sum(nfresh), c = warp_sum(ncand);
-    if (lane == 0) { redi[wid] = a; red[wid] = (double)c; }
+    const int c = warp_sum(ncand);
+    if (lane == 0) redi[wid] = c;
     __syncthreads();
     if (threadIdx.x == 0) {
-      int ta = 0, tc = 0;
-      for (int w = 0; w < nw; ++w) { ta += redi[w]; tc += (int)red[w]; }
-      R.n_refresh = ta;
+      int tc = 0;
+      for (int w = 0; w < nw; ++w) tc += redi[w];
       R.k_candidate = tc;
       const int kf = (flush || sh_err) ? 0 : min(R.k_reuse, tc);
       if (flush) R.k_candidate = 0;
@@ -891,10 +944,35 @@ __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_sel
   }
   const int kfinal = sh_kfinal;
   if (kfinal > 0) {
-    // ascending (E, index) bitonic sort (fusion.py:104-115)
-    if (NP2 >= 64) bitonic_hybrid(ke, ki, NP2);
-    else bitonic_smem(ke, ki, NP2);
-    for (int r = threadIdx.x; r < kfinal; r += blockDim.x) reuse[ki[r]] = 1;
+    // the first K_final candidates of K_D1's ascending (E, index) order:
+    // exclusive scan of the candidate flags along the order
+    const int16_t* ord = kp.order + (size_t)b * N;
+    const int per = (N + blockDim.x - 1) / blockDim.x;
+    const int r0 = threadIdx.x * per, r1 = min(N, r0 + per);
+    int cnt = 0;
+    for (int r = r0; r < r1; ++r) cnt += cand[ord[r]];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) redi[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int w = 0; w < nw; ++w) { const int t = redi[w]; redi[w] = acc; acc += t; }
+    }
+    __syncthreads();
+    int run = redi[wid] + incl - cnt;
+    for (int r = r0; r < r1 && run < kfinal; ++r) {
+      const int q = ord[r];
+      if (cand[q]) {
+        ki[run++] = q;
+        reuse[q] = 1;
+      }
+    }
   }
   __syncthreads();
 

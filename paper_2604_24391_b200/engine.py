@@ -12,7 +12,6 @@ stream, so whole steps can be captured in a CUDA graph.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from dataclasses import dataclass
 
 import torch
@@ -85,9 +84,7 @@ class FreqCacheEngine:
         self.rows = self.height // self.patch_size
         self.cols = self.width // self.patch_size
         self.n_tokens = self.lib.fc_plan_tokens(plan)
-        fast = (self.height, self.width, self.patch_size) == (448, 448, 14)
-        chunk = min(self.batch, max(1, int(os.environ.get("FC_CHUNK", "512"))))
-        self.launches_per_select = (3 * -(-self.batch // chunk) + 1) if fast else 4
+        self.launches_per_select = self.lib.fc_plan_launches(plan)
         sb = self.lib.fc_plan_state_bytes(plan)
         wb = self.lib.fc_plan_workspace_bytes(plan)
         self.state = torch.zeros(sb, dtype=torch.uint8, device=self.device)
@@ -144,12 +141,7 @@ class FreqCacheEngine:
         cols, rows_inv, select) — synchronises; benchmarking only."""
         self._check_frames(frames)
         out = self.out if out is None else out
-        if out.counters is not None and (out.counters.dtype != torch.int64 or out.counters.numel() < 4
-                                         or out.counters.device != self.device):
-            raise ValueError("counters must be an int64 tensor of >= 4 elements on the engine's device")
-        so = nat.SelectOut(out.results.data_ptr(), out.reuse_idx.data_ptr(), out.recompute_idx.data_ptr(),
-                           out.src_map.data_ptr(), out.reuse_mask.data_ptr(), out.refresh_mask.data_ptr(),
-                           out.energy.data_ptr(), out.counters.data_ptr() if out.counters is not None else None)
+        so = self._select_out(out)
         conf = make_config(cfg, refresh_shift)
         with torch.cuda.device(self.device):
             if profile is None:
@@ -161,6 +153,39 @@ class FreqCacheEngine:
                                                 _ptr(self.workspace), C.byref(so), ms, _stream(self.device))
                 profile[:] = list(ms)
         nat.check(rc, "fc_select")
+        return out
+
+    def _select_out(self, out):
+        if out.counters is not None and (out.counters.dtype != torch.int64 or out.counters.numel() < 4
+                                         or out.counters.device != self.device):
+            raise ValueError("counters must be an int64 tensor of >= 4 elements on the engine's device")
+        return nat.SelectOut(out.results.data_ptr(), out.reuse_idx.data_ptr(), out.recompute_idx.data_ptr(),
+                             out.src_map.data_ptr(), out.reuse_mask.data_ptr(), out.refresh_mask.data_ptr(),
+                             out.energy.data_ptr(), out.counters.data_ptr() if out.counters is not None else None)
+
+    def select_front(self, frames, cfg, out, slot, refresh_shift=None):
+        """Front half of a step (``fc_select_front``): energies, refresh mask,
+        token order and row spectra of ``frames`` into workspace ``slot``.
+        Pair with :meth:`select_back` on the same ``out`` and ``slot``; the
+        front of step t + 1 (other slot) may overlap the back of step t."""
+        self._check_frames(frames)
+        so = self._select_out(out)
+        conf = make_config(cfg, refresh_shift)
+        with torch.cuda.device(self.device):
+            rc = self.lib.fc_select_front(self._plan, C.byref(conf), _ptr(frames), _ptr(self.workspace),
+                                          C.byref(so), int(slot), _stream(self.device))
+        nat.check(rc, "fc_select_front")
+        return out
+
+    def select_back(self, cfg, out, slot, refresh_shift=None):
+        """Back half of a step (``fc_select_back``): column FFTs, state swap,
+        phase correlation and the decision, from workspace ``slot``."""
+        so = self._select_out(out)
+        conf = make_config(cfg, refresh_shift)
+        with torch.cuda.device(self.device):
+            rc = self.lib.fc_select_back(self._plan, C.byref(conf), _ptr(self.state), _ptr(self.workspace),
+                                         C.byref(so), int(slot), _stream(self.device))
+        nat.check(rc, "fc_select_back")
         return out
 
     def patch_energy(self, frames, energy=None):
@@ -387,13 +412,18 @@ class StepGraph:
     def __init__(self, fn, device=None):
         self.lib = nat.lib()
         self.device = torch.device(device) if device is not None else torch.device("cuda")
-        st = _stream(self.device)
-        nat.check(self.lib.fc_graph_capture_begin(st), "fc_graph_capture_begin")
-        try:
-            fn()
-        finally:
-            ex = C.c_void_p()
-            rc = self.lib.fc_graph_capture_end(st, C.byref(ex))
+        # the legacy default stream cannot be captured: capture on a side
+        # stream ordered after the caller's work
+        cap = torch.cuda.Stream(self.device)
+        cap.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(cap):
+            st = _stream(self.device)
+            nat.check(self.lib.fc_graph_capture_begin(st), "fc_graph_capture_begin")
+            try:
+                fn()
+            finally:
+                ex = C.c_void_p()
+                rc = self.lib.fc_graph_capture_end(st, C.byref(ex))
         nat.check(rc, "fc_graph_capture_end")
         self._exec = ex
 

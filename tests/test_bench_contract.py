@@ -75,7 +75,8 @@ def test_gpu_arm_json_line():
     read, with self-consistent values."""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--streams", "16", "--steps", "4",
                         "--warmup", "3", "--ring", "4", "--cpu-streams", "2", "--cpu-steps", "1",
-                        "--e2e-steps", "2"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+                        "--e2e-steps", "2", "--sustained-s", "0.2"], capture_output=True, text=True, timeout=900,
+                       cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
     assert len(lines) == 1
@@ -94,3 +95,8 @@ def test_gpu_arm_json_line():
     assert d["e2e_u8"]["h2d_bytes_per_step"] == 16 * 448 * 448 * 3
     assert d["gpu_launches"] > 0 and d["cpu_baseline"]["kind"] in ("port", "reference")
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    assert d["sustained"]["value"] > 0 and d["sustained"]["seconds"] >= 0.16
+    assert "sm_mhz" in d["sustained"]["clocks"]
+    dc = d["decisions"]
+    assert dc["frames"] == 16 * 4 and 0.0 <= dc["reuse_ratio"] <= 1.0 and 0.0 <= dc["flush_rate"] <= 1.0
+    assert d["config"]["graph"] is True

@@ -416,3 +416,37 @@ def test_tensor_store_variants_bit_identical(cuda, monkeypatch):
             assert torch.equal(o.energy, outs[0].energy)
     for e in engines:
         assert torch.equal(e.state, engines[0].state)   # previous-frame spectra, bit for bit
+
+
+@pytest.mark.parametrize("size,streams", [(448, 9), (224, 5), (448, 100)])
+def test_split_phase_pipeline_bit_identical(cuda, size, streams):
+    """fc_select_front / fc_select_back software-pipelined across steps (the
+    front of step t + 1 enqueued on its own stream BEFORE the back of step t,
+    alternating workspace slots, double-buffered outputs) gives exactly the
+    decisions, splice maps and spectrum state of plain fc_select per step —
+    including the small-batch two-lane chunking (100 streams)."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    T = 5
+    frames = torch_stream_frames(streams, T, size, size, seed=77, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    ref = fc.FreqCacheEngine(streams, size, size, 14, fmt="rgb")
+    pip = fc.FreqCacheEngine(streams, size, size, 14, fmt="rgb")
+    outs = [pip.new_output(), pip.new_output()]
+    fs = torch.cuda.Stream()
+    cur = torch.cuda.current_stream()
+    pip.select_front(frames[0], cfg, outs[0], 0, refresh_shift=1)
+    for t in range(T):
+        r = ref.select(frames[t], cfg, refresh_shift=1)
+        fs.wait_stream(cur)
+        if t + 1 < T:
+            with torch.cuda.stream(fs):
+                pip.select_front(frames[t + 1], cfg, outs[(t + 1) & 1], (t + 1) & 1, refresh_shift=1)
+        o = pip.select_back(cfg, outs[t & 1], t & 1, refresh_shift=1)
+        torch.cuda.synchronize()
+        assert torch.equal(o.results, r.results), t
+        for name in ("reuse_idx", "recompute_idx", "src_map", "reuse_mask", "refresh_mask", "energy"):
+            assert torch.equal(getattr(o, name), getattr(r, name)), (t, name)
+        cur.wait_stream(fs)
+    assert torch.equal(pip.state, ref.state)
