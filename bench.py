@@ -415,12 +415,15 @@ def run_ours(a):
     torch.cuda.synchronize()
 
     launches = [0]
-    per_phase = eng.launches_per_select + 2   # + splice plan + copier
+    per_phase = (eng.launches_per_select if a.no_pipeline else eng.launches_per_split_step) + 2  # + splice plan, copier
     main = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_SIDE_PRIO", "-1")))  # splice CTAs jump the select queue
     n_spliced = [0]   # splices issued so far: SpliceState's ping-pong parity
 
-    fs = torch.cuda.Stream(dev)   # front-of-next-step branch
+    # front-of-next-step and back-of-this-step branches (priorities: knobs)
+    fs = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_FRONT_PRIO", "0")))
+    bprio = os.environ.get("FC_BENCH_BACK_PRIO")
+    bs = torch.cuda.Stream(dev, priority=int(bprio)) if bprio is not None else None
 
     def phase(t):
         """Pipelined step t on the current stream, three branches joined at
@@ -443,7 +446,13 @@ def run_ours(a):
             with torch.cuda.stream(fs):
                 eng.select_front(frames[(t + 1) % R], cfg, outs[(t + 1) & 1], (t + 1) & 1,
                                  refresh_shift=a.refresh_shift)
-            eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=a.refresh_shift)
+            if bs is None:
+                eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=a.refresh_shift)
+            else:
+                bs.wait_stream(cur)
+                with torch.cuda.stream(bs):
+                    eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=a.refresh_shift)
+                cur.wait_stream(bs)
         if t > 0:
             with torch.cuda.stream(side):
                 spl.step(outs[(t - 1) & 1].src_map, fresh)

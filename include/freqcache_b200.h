@@ -159,7 +159,9 @@ int  fc_select(const fc_plan* plan, const fc_config* cfg, const void* frames,
  * t + 1 (slot (t + 1) & 1) may run concurrently with the back of step t
  * (slot t & 1) on different streams.  front(slot) then back(slot) on one
  * stream equals fc_select.  Use the same `out` for a step's front and back
- * (the front writes out->energy), and a different one for the next step. */
+ * (the front writes out->energy), and a different one for the next step.
+ * FC_EUNSUPPORTED when the plan's stream chunks outnumber its lanes
+ * (FC_CHUNK / FC_LANES overrides; the defaults always qualify).          */
 int  fc_select_front(const fc_plan* plan, const fc_config* cfg, const void* frames,
                      void* workspace, const fc_select_out* out, int32_t slot,
                      void* cuda_stream);

@@ -50,7 +50,7 @@ struct fc_plan {
   cudaStream_t lanes3[3][kMaxLanes] = {};
   cudaEvent_t fork3[3] = {};
   cudaEvent_t join3[3][kMaxLanes] = {};
-  size_t lane_stride = 0;              // workspace bytes per lane (2 T1 slots + T2)
+  size_t lane_t1 = 0, lane_t2 = 0;     // T1 / T2 bytes of one lane (chunk streams)
   // split-phase select: per-slot strides of the front -> back intermediates
   size_t slot_T = 0, slot_stripes = 0, slot_order = 0, slot_freshm = 0, slot_estats = 0;
   void* fnB = nullptr;                 // K_B / K_C variants (occupancy x twiddle mode)
@@ -252,6 +252,12 @@ void launch_rank(const fc_plan* pl, const fc_config& cfg, const KParams& kp, int
   if (rec) rec->mark(after, 3);
 }
 
+// The split-phase front writes every chunk's row spectra before the back
+// reads them: each chunk needs its own T1 buffers (chunks <= lanes).
+bool split_ok(const fc_plan* pl) {
+  return !pl->fast || (pl->g.batch + pl->chunk - 1) / pl->chunk <= pl->lanes;
+}
+
 // Which kernels a call launches: the whole select, or one half of the
 // split-phase select (front: K_A + K_D1 of a step; back: K_B + K_C + K_D).
 enum Part { kAll = 0, kFront = 1, kBack = 2 };
@@ -278,31 +284,37 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
     CUtensorMap tm1[kMaxLanes], tm2[kMaxLanes];
     std::memset(tm1, 0, sizeof(tm1));
     std::memset(tm2, 0, sizeof(tm2));
-    const int nmaps = rec ? 1 : pl->lanes;
-    for (int l = 0; l < nmaps; ++l) {
-      uint8_t* t1 = reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride;
-      uint8_t* t2 = reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride;
-      if (front && pl->t1_tma && !encode_t1_map(&tm1[l], t1, pl->chunk)) return FC_ECUDA;
-      if (back && pl->t2_tma && !encode_t2_map(&tm2[l], t2, pl->chunk)) return FC_ECUDA;
+    // the split-phase halves overlap each other across steps already: they
+    // launch the whole batch as one chunk (FC_SPLIT_LANES=1: the plan's
+    // chunks on its lanes)
+    static const int split_lanes = env_int("FC_SPLIT_LANES", 0, 0, 1);
+    const bool whole = part != kAll && !split_lanes;
+    const int chunk = whole ? B : pl->chunk;
+    const int nmap = whole ? 1 : pl->lanes;
+    for (int l = 0; l < nmap; ++l) {
+      uint8_t* t1 = reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_t1;
+      uint8_t* t2 = reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_t2;
+      if (front && pl->t1_tma && !encode_t1_map(&tm1[l], t1, chunk)) return FC_ECUDA;
+      if (back && pl->t2_tma && !encode_t2_map(&tm2[l], t2, chunk)) return FC_ECUDA;
     }
     // Chunks of `chunk` streams run A -> B -> C on `lanes` internal streams
     // (each lane owns its T1/T2 slice) so one chunk's tail overlaps the next
     // chunk's head; the caller stream forks to and joins from the lanes.
     // Profiling runs the chunks serially on the caller stream.
     auto fa = (FastRowsFwd)sel_fast_rows_fwd(pl->g.format, pl->t1_tma);
-    const int nl = rec ? 1 : pl->lanes;
+    const int nl = (rec || whole) ? 1 : pl->lanes;
     if (!rec) {
       cudaEventRecord(set.fork, st);
       for (int l = 0; l < nl; ++l) cudaStreamWaitEvent(set.lane[l], set.fork, 0);
     }
     int c = 0;
-    for (int b0 = 0; b0 < B; b0 += pl->chunk, ++c) {
-      const int nb = B - b0 < pl->chunk ? B - b0 : pl->chunk;
-      const int l = c % nl;
-      const cudaStream_t ls = rec ? st : set.lane[l];
+    for (int b0 = 0; b0 < B; b0 += chunk, ++c) {
+      const int nb = B - b0 < chunk ? B - b0 : chunk;
+      const int l = whole ? 0 : c % pl->lanes;   // the lane's T1 / T2 buffers
+      const cudaStream_t ls = rec ? st : set.lane[c % nl];
       KParams kl = kp;
-      kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_stride);
-      kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_stride);
+      kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_t1);
+      kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_t2);
       if (front) {
         fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1, tm1[l]);
         if (rec) rec->mark(st, 0);
@@ -427,14 +439,14 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     pl->smemC = (size_t)kSmemC448;
     kp.NCB = kNCB448;   // K_B stats partials per stream
     kp.NRG = kNRG448;   // K_C peak partials per stream
-    const size_t ch = pl->chunk;
-    const size_t t1 = align_up(ch * 224 * 448 * sizeof(float2));
-    const size_t t2 = align_up(ch * 448 * 224 * sizeof(float2));
-    pl->lane_stride = 2 * t1 + t2;   // [T1 slot 0 | T1 slot 1 | T2] per lane
+    // [T1 slot 0: lanes x chunk streams | T1 slot 1 | T2], lanes contiguous
+    // inside each, so a launch over the whole batch can also address them
+    pl->lane_t1 = (size_t)pl->chunk * 224 * 448 * sizeof(float2);
+    pl->lane_t2 = (size_t)pl->chunk * 448 * 224 * sizeof(float2);
     pl->off_T = off;
-    pl->off_T2 = off + 2 * t1;
-    pl->slot_T = t1;
-    off += pl->lane_stride * pl->lanes;
+    pl->slot_T = align_up(pl->lane_t1 * pl->lanes);
+    pl->off_T2 = off + 2 * pl->slot_T;
+    off = pl->off_T2 + align_up(pl->lane_t2 * pl->lanes);
     specElems = B * 224 * kStCol * 2;  // register-order state (float2 count)
   } else {
     pl->chunk = g.batch;
@@ -622,6 +634,7 @@ int fc_select_front(const fc_plan* pl, const fc_config* cfg, const void* frames,
     return FC_EINVAL;
   const int rc = check_cfg(cfg);
   if (rc != FC_OK) return rc;
+  if (!split_ok(pl)) return FC_EUNSUPPORTED;
   const KParams kp = bind(pl, nullptr, ws, out->energy, slot);
   const int lrc = launch_select(pl, *cfg, frames, kp, *out, as_stream(stream), nullptr, kFront);
   if (lrc != FC_OK) return lrc;
@@ -634,6 +647,7 @@ int fc_select_back(const fc_plan* pl, const fc_config* cfg, void* state, void* w
   if ((reinterpret_cast<uintptr_t>(state) | reinterpret_cast<uintptr_t>(ws)) & 15) return FC_EINVAL;
   const int rc = check_cfg(cfg);
   if (rc != FC_OK) return rc;
+  if (!split_ok(pl)) return FC_EUNSUPPORTED;
   const KParams kp = bind(pl, state, ws, out->energy, slot);
   const int lrc = launch_select(pl, *cfg, nullptr, kp, *out, as_stream(stream), nullptr, kBack);
   if (lrc != FC_OK) return lrc;

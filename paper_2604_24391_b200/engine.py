@@ -12,6 +12,7 @@ stream, so whole steps can be captured in a CUDA graph.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import torch
@@ -85,6 +86,10 @@ class FreqCacheEngine:
         self.cols = self.width // self.patch_size
         self.n_tokens = self.lib.fc_plan_tokens(plan)
         self.launches_per_select = self.lib.fc_plan_launches(plan)
+        # select_front + select_back of one step: K_A, K_D1 | K_B, K_C, K_D
+        # over the whole batch (FC_SPLIT_LANES=1: the plan's chunks instead)
+        self.launches_per_split_step = (self.launches_per_select
+                                        if os.environ.get("FC_SPLIT_LANES") == "1" else 5)
         sb = self.lib.fc_plan_state_bytes(plan)
         wb = self.lib.fc_plan_workspace_bytes(plan)
         self.state = torch.zeros(sb, dtype=torch.uint8, device=self.device)
