@@ -466,7 +466,7 @@ def run_ours(a):
         fr = frames[t % R]
         prof = []
         out = eng.select(fr, cfg, refresh_shift=a.refresh_shift, profile=prof)
-        for k in range(4):
+        for k in range(5):
             kernel_ms[k] += prof[k]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -474,7 +474,7 @@ def run_ours(a):
         n_spliced[0] += 1
         e1.record()
         torch.cuda.synchronize()
-        kernel_ms[4] += e0.elapsed_time(e1)
+        kernel_ms[5] += e0.elapsed_time(e1)
         # bytes the splice actually moves this step: in-place streams only
         # their recomputed rows, shifted streams every row
         r = out.host_results()
@@ -587,8 +587,8 @@ def run_ours(a):
 
     # ---- per-kernel timing pass (same steps, events between launches)
     kp_steps = min(a.steps, 16)
-    names = ["rows_fwd", "cols", "rows_inv", "select", "splice"]
-    kms = [0.0] * 5
+    names = ["rows_fwd", "cols", "rows_inv", "select", "rank", "splice"]
+    kms = [0.0] * 6
     t0 = t_next
     for t in range(t0, t0 + kp_steps):
         one_step(t, kms)
@@ -597,33 +597,43 @@ def run_ours(a):
     hw = H * H
     spec = 8 * H * ((H // 2 + 7) // 8) * 8   # one packed half-spectrum, fp32 complex
     kbytes = [
-        S * (12 * hw + spec + 8 * N),          # rows_fwd: RGB in, packed rows (T1) out, energies
-        S * (4 * spec),                        # cols: T1 in, state in/out, T2 out
-        S * spec,                              # rows_inv: T2 in
-        S * (8 * N + 14 * N + 136),            # select: energies in, masks/indices out
+        S * (12 * hw + spec + 8 * N),          # rows_fwd K_A: RGB in, packed rows (T1) out, energies
+        S * (4 * spec),                        # cols K_B: T1 in, state in/out, T2 out
+        S * spec,                              # rows_inv K_C: T2 in
+        S * (3 * N + 14 * N + 136),            # select K_D: order + refresh mask in, masks/indices out
+        S * (8 * N + 3 * N + 32),              # rank K_D1: energies in, order + refresh mask + stats out
         splice_moved,                          # splice: rows it must move (recomputed / shifted), map, ages
     ]
-    dom = max(range(5), key=lambda k: kms[k])
+    nk = len(names)
+    dom = max(range(nk), key=lambda k: kms[k])
     hbm, peak_kind = peaks()
     ach = kbytes[dom] / (kms[dom] / 1e3) / 1e9
     b_sel = 20 * hw + 16 * N
     b_spl = 4 * N * D + 20 * N
-    step_ach = (b_sel + b_spl) * (S * a.steps) / (ms / 1e3) / 1e9 if world == 1 else \
-        (b_sel + b_spl) * value / world / 1e9
+    frames_per_s_gpu = (S * a.steps) / (ms / 1e3) if world == 1 else value / world
+    step_ach = (b_sel + b_spl) * frames_per_s_gpu / 1e9
+    moved_ach = (b_sel + splice_moved / S) * frames_per_s_gpu / 1e9
     roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "traffic": None, "kernel": names[dom], "peak_kind": peak_kind,
                 "bytes_per_launch": kbytes[dom], "ms_per_launch": kms[dom]}
     roofline_step = {"bound": "hbm", "achieved": step_ach, "peak": hbm, "unit": "GB/s", "frac": step_ach / hbm,
                      "bytes_per_frame": b_sel + b_spl, "select_bytes": b_sel, "splice_bytes": b_spl,
                      "splice_moved_bytes_per_frame": splice_moved / S,
+                     "achieved_moved": moved_ach, "frac_moved": moved_ach / hbm,
                      "note": "SURVEY 8(d) algorithmic bytes; the in-place splice moves only recomputed "
-                             "rows of zero-displacement streams (splice_moved_bytes_per_frame)"}
+                             "rows of zero-displacement streams: frac_moved counts the select bytes plus "
+                             "the splice bytes actually moved"}
     kernels = {names[k]: {"ms": kms[k], "share": kms[k] / sum(kms), "bytes": kbytes[k],
-                          "gbs": kbytes[k] / (kms[k] / 1e3) / 1e9} for k in range(5)}
+                          "gbs": kbytes[k] / (kms[k] / 1e3) / 1e9} for k in range(nk)}
+    # ncu DRAM bytes per launch of the same kernel, from the capture named in
+    # profiles/traffic.json (tagged with its capture id: it is not re-measured
+    # by this run)
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f)
-        roofline["traffic"] = tr.get(names[dom])
+        if isinstance(tr.get("kernels"), dict) and tr["kernels"].get(names[dom]) is not None:
+            roofline["traffic"] = tr["kernels"][names[dom]]
+            roofline["traffic_capture"] = tr.get("capture")
     except (OSError, ValueError):
         pass
 

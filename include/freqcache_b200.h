@@ -171,8 +171,9 @@ int  fc_select_back(const fc_plan* plan, const fc_config* cfg, void* state,
 
 /* fc_select with a CUDA event after every launch, all launches serial on
  * the caller's stream; synchronises and returns per-kernel-kind device time
- * in kernel_ms[4] (rows_fwd, cols, rows_inv, select = K_D1 + K_D), summed
- * over stream chunks.  For benchmarking. */
+ * in kernel_ms[5] (rows_fwd K_A, cols K_B, rows_inv K_C, select K_D, rank
+ * K_D1), summed over stream chunks.  For benchmarking and the facade's
+ * per-stage timings_us. */
 int  fc_select_profile(const fc_plan* plan, const fc_config* cfg, const void* frames,
                        void* state, void* workspace, const fc_select_out* out,
                        float* kernel_ms, void* cuda_stream);
@@ -269,6 +270,28 @@ int  fc_compare_cosines(const fc_geometry* geom, const void* prev, const void* c
  * custom token_fn's vectors.                                                */
 int  fc_row_cosines(int64_t n, int64_t d, const double* a, const double* b,
                     double* out, void* cuda_stream);
+
+/* ---- fp64 transform wrappers (spectral.py:24-72, migration.py:128-134):
+ * the reference's public transform API, on the GPU in fp64 (dense passes
+ * with exact twiddles; not the decision path's packed fp32 FFTs).  Complex
+ * grids are interleaved (re, im) float64, row-major [h][w].                 */
+int64_t fc_dft2_workspace_bytes(int32_t h, int32_t w);
+/* out = fft2(in) (inverse == 0, unnormalised) or ifft2(in) (scaled 1/(h w));
+ * in is real [h][w] (in_complex == 0) or complex.  dft2 / idft2.            */
+int  fc_dft2(int32_t h, int32_t w, const double* in, int32_t in_complex,
+             int32_t inverse, double* out, void* workspace, void* cuda_stream);
+int64_t fc_phase_correlation_workspace_bytes(int32_t h, int32_t w);
+/* phase_correlation_spectra: normalised cross-power, ifft2, argmax with the
+ * reference tie rule -> disp2 = (di, dj) pixels (device int32[2])          */
+int  fc_phase_correlation_spectra(int32_t h, int32_t w, const double* spec_prev,
+                                  const double* spec_curr, int32_t* disp2,
+                                  void* workspace, void* cuda_stream);
+/* block_dct: orthonormal 2-D DCT-II of n square p x p patches (p <= 64)     */
+int  fc_block_dct(int32_t n_patches, int32_t p, const double* patches,
+                  double* out, void* cuda_stream);
+/* amplitude_phase: |z| and atan2(Im z, Re z) of n complex values            */
+int  fc_amplitude_phase(int64_t n, const double* spectrum, double* amp,
+                        double* phase, void* cuda_stream);
 
 /* ---- CUDA-graph capture of whole steps (runtime plumbing, not an op of the
  * reference).  Capture everything a step launches on `cuda_stream` (other

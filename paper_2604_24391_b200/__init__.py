@@ -48,9 +48,11 @@ from .api import (  # noqa: F401
     refresh_mask,
     run_sequence,
     sim_freq,
+    sim_spatial,
     spectral_entropy,
     step,
     topk_ascending,
 )
+from .spectral import amplitude_phase, block_dct, dft2, idft2, phase_correlation_spectra  # noqa: F401
 from .engine import FreqCacheEngine, SelectResult, SpliceState, StepGraph, splice, splice_map  # noqa: F401
 from . import records  # noqa: F401

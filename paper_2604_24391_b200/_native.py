@@ -47,6 +47,8 @@ EXPORTS = (
     "fc_refresh_mask", "fc_topk_ascending", "fc_render_masks", "fc_splice_packed",
     "fc_splice_inplace", "fc_splice_inplace_scratch_bytes", "fc_compare_cosines", "fc_row_cosines",
     "fc_graph_capture_begin", "fc_graph_capture_end", "fc_graph_launch", "fc_graph_destroy",
+    "fc_dft2_workspace_bytes", "fc_dft2", "fc_phase_correlation_workspace_bytes", "fc_phase_correlation_spectra",
+    "fc_block_dct", "fc_amplitude_phase",
 )
 
 
@@ -133,6 +135,12 @@ def load(path=None):
         "fc_graph_capture_end": (C.c_int, [vp, C.POINTER(vp)]),
         "fc_graph_launch": (C.c_int, [vp, vp]),
         "fc_graph_destroy": (None, [vp]),
+        "fc_dft2_workspace_bytes": (i64, [i32, i32]),
+        "fc_dft2": (C.c_int, [i32, i32, vp, i32, i32, vp, vp, vp]),
+        "fc_phase_correlation_workspace_bytes": (i64, [i32, i32]),
+        "fc_phase_correlation_spectra": (C.c_int, [i32, i32, vp, vp, vp, vp, vp]),
+        "fc_block_dct": (C.c_int, [i32, i32, vp, vp, vp]),
+        "fc_amplitude_phase": (C.c_int, [i64, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -85,6 +85,21 @@ def decision_from_device(res, reuse_idx, recompute_idx, refresh_mask, step=0, ti
     )
 
 
+def stage_timings(prof):
+    """Per-stage device microseconds of one profiled select in the
+    reference's ``timings_us`` keys (fusion.py:137-221).  The kernels fuse
+    stages, so each key holds the kernel that carries the stage's main work:
+    transform = luma + block-DCT energies + row FFTs (K_A) and column FFTs
+    (K_B, which also accumulates the similarity / entropy sums); migration =
+    inverse row FFTs + impulse argmax (K_C); edge = energy statistics,
+    refresh mask and token order (K_D1); budget = entropy / alpha / K (a few
+    scalar instructions inside K_D; its sums are counted under transform);
+    select = candidates, top-K and outputs (K_D)."""
+    us = [1e3 * v for v in prof]
+    return {"transform": int(us[0] + us[1]), "migration": int(us[2]), "edge": int(us[4]), "budget": 0,
+            "select": int(us[3]), "device": int(sum(us))}
+
+
 def _fetch(out, row=0):
     res = out.host_results()[row]
     ri = out.reuse_idx[row].cpu().numpy()
@@ -126,19 +141,16 @@ def decide(prev, curr, cfg, *, step=0, parallel=False):
     first = getattr(eng, "_aux_out", None)
     if first is None:
         first = eng._aux_out = eng.new_output()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tp, tc = _device_frame(prev), _device_frame(curr)
-    start.record()
     eng.reset()
     eng.select(tp, cfg, out=first)
-    out = eng.select(tc, cfg)
-    end.record()
+    prof = []
+    out = eng.select(tc, cfg, profile=prof)
     res0 = first.host_results()[0]
     _raise_status(res0)
     res, ri, rc, rm = _fetch(out)
     _raise_status(res)
-    d = decision_from_device(res, ri, rc, rm, step=step,
-                             timings={"device": int(start.elapsed_time(end) * 1000)})
+    d = decision_from_device(res, ri, rc, rm, step=step, timings=stage_timings(prof))
     assert_decision(d, rows * cols)
     return d
 
@@ -240,10 +252,11 @@ def run_sequence(frames, cfg, token_fn=default_token_fn, cost_model=None, parall
     _raise_status(aux.host_results()[0])
     decisions, reports = [], []
     for t in range(1, len(frames)):
-        out = eng.select(_device_frame(frames[t]), cfg)
+        prof = []
+        out = eng.select(_device_frame(frames[t]), cfg, profile=prof)
         res, ri, rc, rm = _fetch(out)
         _raise_status(res)
-        d = decision_from_device(res, ri, rc, rm, step=t)
+        d = decision_from_device(res, ri, rc, rm, step=t, timings=stage_timings(prof))
         assert_decision(d, n)
         grid = PatchGrid(frames[t], p)
         fresh = _fresh_rows(grid, d.recompute_set, token_fn)
@@ -417,3 +430,31 @@ def topk_ascending(candidates, energies, k):
     if int(flags.item()) & 4:
         raise IndexError("candidate index out of range")
     return tuple(int(v) for v in out.cpu().tolist())
+
+
+def sim_spatial(prev, curr, grid, token_fn):
+    """Mean position-wise cosine of patch embeddings — the visual-domain
+    baseline score (migration.py:53-84).  ``token_fn`` is host model code as
+    in the reference; the cosines run on the GPU (``fc_row_cosines``, fp64).
+    Zero-norm pairs contribute 0 and trigger a RuntimeWarning."""
+    import warnings
+
+    from .engine import row_cosines
+    from .geometry import validate_frame
+
+    prev = validate_frame(prev)
+    curr = validate_frame(curr)
+    if prev.shape != curr.shape:
+        raise ValueError(f"frame shapes differ: {prev.shape} vs {curr.shape}")
+    pos = [(i, j) for i in range(grid.rows) for j in range(grid.cols)]
+    a = np.stack([np.asarray(token_fn(grid.patch(i, j, prev)), dtype=np.float64).ravel() for i, j in pos])
+    b = np.stack([np.asarray(token_fn(grid.patch(i, j, curr)), dtype=np.float64).ravel() for i, j in pos])
+    cos = row_cosines(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+    degenerate = int(((np.linalg.norm(a, axis=1) == 0.0) | (np.linalg.norm(b, axis=1) == 0.0)).sum())
+    if degenerate:
+        warnings.warn(f"{degenerate} patch position(s) had zero-norm embeddings and contributed 0 similarity",
+                      RuntimeWarning, stacklevel=2)
+    total = 0.0
+    for c in cos:
+        total += float(c)
+    return total / grid.n_patches

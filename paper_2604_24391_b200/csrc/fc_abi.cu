@@ -23,6 +23,7 @@
 #include "fc_fast448w.cuh"
 #include "fc_compare.cuh"
 #include "fc_stages.cuh"
+#include "fc_spectral.cuh"
 
 namespace {
 constexpr int kChunkDefault = 512;  // streams per A/B/C launch group on the fast path
@@ -249,7 +250,7 @@ void launch_rank(const fc_plan* pl, const fc_config& cfg, const KParams& kp, int
   }
   if (nb <= kSmallBatch) k_rank<512><<<nb, 512, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
   else k_rank<FC_SEL_THREADS><<<nb, FC_SEL_THREADS, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
-  if (rec) rec->mark(after, 3);
+  if (rec) rec->mark(after, 4);
 }
 
 // The split-phase front writes every chunk's row spectra before the back
@@ -676,11 +677,11 @@ int fc_select_profile(const fc_plan* pl, const fc_config* cfg, const void* frame
   rc = launch_select(pl, *cfg, frames, kp, *out, st, &r);
   if (rc == FC_OK) rc = launch_check();
   cudaStreamSynchronize(st);
-  for (int k = 0; k < 4; ++k) kernel_ms[k] = 0.f;
+  for (int k = 0; k < 5; ++k) kernel_ms[k] = 0.f;
   for (int i = 1; i < r.n; ++i) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
-    if (kind[i] >= 0 && kind[i] < 4) kernel_ms[kind[i]] += ms;
+    if (kind[i] >= 0 && kind[i] < 5) kernel_ms[kind[i]] += ms;
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return rc;
@@ -879,6 +880,88 @@ int fc_splice_map(int32_t rows, int32_t cols, const int32_t* reuse_idx, int32_t 
       return FC_ECUDA;
   }
   k_splice_map<<<1, 512, smem, as_stream(stream)>>>(rows, cols, reuse_idx, k, dip, djp, src_map, flag);
+  return launch_check();
+}
+
+// ------------------------------------------------- fp64 spectral wrappers ----
+// spectral.py:24-72 and migration.py:128-134 on the GPU (fc_spectral.cuh).
+
+static size_t a256(size_t v) { return (v + 255) / 256 * 256; }
+
+int64_t fc_dft2_workspace_bytes(int32_t h, int32_t w) {
+  if (h < 1 || w < 1) return -1;
+  return (int64_t)(a256((size_t)h * w * 16) + a256((size_t)w * 16) + a256((size_t)h * 16));
+}
+
+static int dft2_impl(int h, int w, const double* in, int in_complex, int inverse, double* out, uint8_t* ws,
+                     cudaStream_t st) {
+  double2* Y = reinterpret_cast<double2*>(ws);
+  double2* twW = reinterpret_cast<double2*>(ws + a256((size_t)h * w * 16));
+  double2* twH = reinterpret_cast<double2*>(reinterpret_cast<uint8_t*>(twW) + a256((size_t)w * 16));
+  const int sign = inverse ? 1 : -1;
+  spec::k_twiddles<<<(w + 255) / 256, 256, 0, st>>>(w, sign, twW);
+  spec::k_twiddles<<<(h + 255) / 256, 256, 0, st>>>(h, sign, twH);
+  const size_t smem = (size_t)w * 32;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute((void*)spec::k_dft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+    return FC_ECUDA;
+  spec::k_dft_rows<<<dim3((w + spec::kThreads - 1) / spec::kThreads, h), spec::kThreads, smem, st>>>(
+      h, w, in, in_complex, twW, Y);
+  const double scale = inverse ? 1.0 / ((double)h * (double)w) : 1.0;
+  spec::k_dft_cols<<<dim3((w + spec::kThreads - 1) / spec::kThreads, (h + spec::kTK - 1) / spec::kTK),
+                     spec::kThreads, 0, st>>>(h, w, Y, twH, scale, out);
+  return launch_check();
+}
+
+int fc_dft2(int32_t h, int32_t w, const double* in, int32_t in_complex, int32_t inverse, double* out, void* ws,
+            void* stream) {
+  if (h < 1 || w < 1 || h > 8192 || w > 6144 || !in || !out || !ws) return FC_EINVAL;
+  return dft2_impl(h, w, in, in_complex, inverse, out, static_cast<uint8_t*>(ws), as_stream(stream));
+}
+
+int64_t fc_phase_correlation_workspace_bytes(int32_t h, int32_t w) {
+  const int64_t d = fc_dft2_workspace_bytes(h, w);
+  if (d < 0) return -1;
+  return d + 2 * (int64_t)a256((size_t)h * w * 16) + (int64_t)a256(1024 * sizeof(spec::PeakD));
+}
+
+int fc_phase_correlation_spectra(int32_t h, int32_t w, const double* spec_prev, const double* spec_curr,
+                                 int32_t* disp2, void* ws, void* stream) {
+  if (h < 1 || w < 1 || h > 8192 || w > 6144 || !spec_prev || !spec_curr || !disp2 || !ws) return FC_EINVAL;
+  const cudaStream_t st = as_stream(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  const size_t grid = a256((size_t)h * w * 16);
+  double* cross = reinterpret_cast<double*>(base + fc_dft2_workspace_bytes(h, w));
+  double* resp = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(cross) + grid);
+  spec::PeakD* parts = reinterpret_cast<spec::PeakD*>(reinterpret_cast<uint8_t*>(resp) + grid);
+  const int64_t n = (int64_t)h * w;
+  const int nb = (int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+  spec::k_cross_power<<<nb, 256, 0, st>>>(n, spec_prev, spec_curr, 1e-12, cross);   // CROSS_POWER_EPS
+  int rc = dft2_impl(h, w, cross, 1, 1, resp, base, st);
+  if (rc != FC_OK) return rc;
+  spec::k_peak_part<<<nb, spec::kThreads, 0, st>>>(h, w, resp, parts);
+  spec::k_peak_fin<<<1, spec::kThreads, 0, st>>>(h, w, parts, nb, disp2);
+  return launch_check();
+}
+
+int fc_block_dct(int32_t n_patches, int32_t p, const double* patches, double* out, void* stream) {
+  if (n_patches < 0 || p < 1 || p > 64 || (n_patches > 0 && (!patches || !out))) return FC_EINVAL;
+  if (n_patches == 0) return FC_OK;
+  const size_t smem = (size_t)3 * p * p * sizeof(double);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute((void*)spec::k_block_dct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+    return FC_ECUDA;
+  spec::k_block_dct<<<n_patches, spec::kThreads, smem, as_stream(stream)>>>(p, patches, out);
+  return launch_check();
+}
+
+int fc_amplitude_phase(int64_t n, const double* spectrum, double* amp, double* phase, void* stream) {
+  if (n < 0 || (n > 0 && (!spectrum || !amp || !phase))) return FC_EINVAL;
+  if (n == 0) return FC_OK;
+  const int nb = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  spec::k_amp_phase<<<nb, 256, 0, as_stream(stream)>>>(n, spectrum, amp, phase);
   return launch_check();
 }
 

@@ -143,7 +143,7 @@ class FreqCacheEngine:
     def select(self, frames, cfg, out=None, refresh_shift=None, profile=None):
         """One decision step for every stream; returns device outputs.
         ``profile``: a list that receives per-kernel device ms (rows_fwd,
-        cols, rows_inv, select) — synchronises; benchmarking only."""
+        cols, rows_inv, select, rank) — launches serially and synchronises."""
         self._check_frames(frames)
         out = self.out if out is None else out
         so = self._select_out(out)
@@ -153,7 +153,7 @@ class FreqCacheEngine:
                 rc = self.lib.fc_select(self._plan, C.byref(conf), _ptr(frames), _ptr(self.state),
                                         _ptr(self.workspace), C.byref(so), _stream(self.device))
             else:
-                ms = (C.c_float * 4)()
+                ms = (C.c_float * 5)()
                 rc = self.lib.fc_select_profile(self._plan, C.byref(conf), _ptr(frames), _ptr(self.state),
                                                 _ptr(self.workspace), C.byref(so), ms, _stream(self.device))
                 profile[:] = list(ms)

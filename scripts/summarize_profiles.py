@@ -22,7 +22,7 @@ ROOT = Path(__file__).resolve().parent.parent
 OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
 NAMES = {"k448_rows_fwd": "rows_fwd", "k448_cols": "cols", "k448_rows_inv": "rows_inv",
-         "k_select": "select", "k_splice16": "splice", "k_splice_ip": "splice", "k_splice_ip_bulk": "splice",
+         "k_select": "select", "k_rank": "rank", "k_splice16": "splice", "k_splice_ip": "splice", "k_splice_ip_bulk": "splice",
          "k_splice_plan": "splice_plan"}
 
 
@@ -122,7 +122,9 @@ def main(tag):
     traffic = {k: sum(v) / len(v) for k, v in traffic.items()}
     if "splice_plan" in traffic and "splice" in traffic:
         traffic["splice"] += traffic.pop("splice_plan")
-    (PROF / "traffic.json").write_text(json.dumps(traffic, indent=1))
+    (PROF / "traffic.json").write_text(json.dumps(
+        {"capture": f"{tag} (profiles/{tag}_ncu_raw.csv): dram__bytes_read.sum + dram__bytes_write.sum per launch",
+         "kernels": traffic}, indent=1))
     print("\n".join(lines))
 
 

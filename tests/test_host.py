@@ -23,7 +23,7 @@ def lib():
 
 def test_library_exports_every_header_symbol(lib):
     hdr = (ROOT / "include" / "freqcache_b200.h").read_text()
-    decl = set(re.findall(r"\b(fc_[a-z_]+)\s*\(", hdr))
+    decl = set(re.findall(r"\b(fc_[a-z0-9_]+)\s*\(", hdr))
     assert decl, "no declarations parsed"
     from paper_2604_24391_b200 import _native
     assert decl == set(_native.EXPORTS)
