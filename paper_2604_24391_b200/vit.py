@@ -9,13 +9,13 @@ hidden-state splice are this package's sm_100a kernels.
 
 Two cached-step modes (``CachedEncoder.step``):
 
-* ``"layer1"`` — the config's literal wording: the cache holds each token's
-  patch-embedding state (layer 0) and first-block output (layer 1).  Only
-  recomputed tokens go through the patch embedding and block 1 (queries =
-  recomputed tokens; keys/values = all tokens, reused ones from the
-  displacement-mapped layer-0 cache); the block-1 outputs are spliced with
-  the cached ones and blocks 2..27 run on all tokens.  Savings are bounded by
-  block 1's share of the encoder (~3.7 %).
+* ``"layer1"`` — the config's literal wording: only recomputed tokens go
+  through the patch embedding and the first block; the cache holds each
+  token's first-block keys / values and output.  Queries = recomputed
+  tokens; keys/values = all tokens (reused ones from the displacement-mapped
+  K/V cache); the first-block outputs are spliced with the cached ones and
+  blocks 2..27 run on all tokens.  Savings are bounded by the first block's
+  share of the encoder (~3.7 %).
 * ``"subset"`` — the deployment-style reading: the cache holds final hidden
   states; recomputed tokens run the whole encoder attending among
   themselves, reused tokens take their (displacement-mapped) cached final
@@ -23,13 +23,14 @@ Two cached-step modes (``CachedEncoder.step``):
   ([sum K_b, D] GEMMs, jagged-nested SDPA per stream), so the encoder work
   scales with the recompute ratio.
 
-Both splice through ``fc_splice`` (bf16, bit copies) with the select's
-``src_map``, and both report the cosine similarity of their output to a full
-recompute of the same frame.
+Both splice through ``fc_splice`` (bf16, bit copies, device-side bounds
+check) with the select's ``src_map``, and both report the cosine similarity
+of their output to a full recompute of the same frame.
 """
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -148,83 +149,238 @@ class ViT(torch.nn.Module):
         return self.ln(x)
 
 
-def _gather_rows(x, idx):
-    """x [B, N, D], idx [B, K] (-1 padded) -> [B, K, D] (padding rows = 0)."""
-    safe = idx.clamp_min(0).long()
-    out = torch.gather(x, 1, safe[..., None].expand(-1, -1, x.shape[-1]))
-    return out * (idx >= 0)[..., None].to(out.dtype)
-
-
 class CachedEncoder:
-    """Batched token-cache encoder over B streams (select + partial ViT + splice)."""
+    """Batched token-cache encoder over B streams (select + partial ViT + splice).
 
-    def __init__(self, model: ViT, batch: int, mode: str = "layer1", device="cuda", group: int = 0):
+    Host synchronisation: the only values the host needs (the recompute
+    count of every stream, which sizes the recompute bucket and the packed
+    batch) come from the select's results record.  The select of the next
+    step can be issued ahead (``step(..., next_frames=...)``) on a side
+    stream, so by the time the host reads those counts the select has long
+    finished and the device queue still holds the previous step's encoder
+    blocks — the host waits on the select's event, never on the encoder.
+
+    Recomputed tokens of all streams are packed without padding ([sum K_b, D]
+    rows), so the partial work scales with the recompute ratio of each
+    stream rather than the worst stream's.
+
+    ``layer1`` caches every token's block-0 q | k | v row and block-0 output
+    (displacement-mapped like the tokens): recomputed tokens run the patch
+    embedding, LN and the QKV projection, their fresh q | k | v rows are
+    spliced into the cache (``fc_splice_packed``, one 3D-wide row per token),
+    one dense attention runs over all tokens of each stream (library SDPA:
+    cheaper on B200 than a variable-length kernel for the recomputed queries
+    only) and only the recomputed rows go on through the projection and the
+    MLP; the block-0 outputs are spliced with the cached ones and blocks
+    1..26 run on every token, replayed from a CUDA graph (static shapes).
+    Reused tokens skip the embedding, block-0 QKV, projection and MLP.
+    """
+
+    def __init__(self, model: ViT, batch: int, mode: str = "layer1", device="cuda", group: int = 0,
+                 graphs: bool = True):
         if mode not in ("layer1", "subset"):
             raise ValueError(mode)
         c = model.c
         self.m, self.mode, self.B, self.group = model, mode, batch, (group or batch)
+        self.device = torch.device(device)
         self.engine = FreqCacheEngine(batch, c.image, c.image, c.patch, fmt="rgb", device=device)
         n, d = c.tokens, c.width
         dt = next(model.parameters()).dtype
-        self.h1 = torch.zeros((2, batch, n, d), dtype=dt, device=device)   # cached layer-1 / final
-        self.h0 = torch.zeros((2, batch, n, d), dtype=dt, device=device)   # cached layer-0 (layer1 mode)
+        self.h1 = torch.zeros((2, batch, n, d), dtype=dt, device=device)   # cached block-0 output / final
+        if mode == "layer1":
+            # cached block-0 q | k | v rows of every token (one 3D-wide row per token)
+            self.qkv0 = torch.zeros((2, batch, n, 3 * d), dtype=dt, device=device)
+        self.tail_graphs = {} if (graphs and mode == "layer1") else None
+        self._tail_out = {}
         self.ages = torch.zeros((2, batch, n), dtype=torch.int64, device=device)
+        self.scratch_ages = torch.zeros((batch, n), dtype=torch.int64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)      # splice bounds flag
         self.cur = 0
+        # select results double-buffered; counts to the host through pinned memory
+        self.outs = [self.engine.new_output(), self.engine.new_output()]
+        self.sel_stream = torch.cuda.Stream(self.device)
+        self.select_on_main = os.environ.get("FC_VIT_SELECT_MAIN") == "1"   # diagnostics knob
+        self.debug_marks = None   # diagnostics: a list receives per-step (start, block 0 done, tail done) events
+        self.host_counts = [torch.zeros(batch, dtype=torch.int32).pin_memory() for _ in range(2)]
+        # packed-row offsets per select slot, built on the device (no
+        # per-step pinned allocations: those can synchronise the device)
+        self.offsets = [torch.zeros(batch + 1, dtype=torch.int64, device=device) for _ in range(2)]
+        self.sel_done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.pending = None   # (frames tensor, slot) of a select issued ahead
+        self.k = 0
+        if self.tail_graphs is not None:   # capture both tail graphs up front
+            with torch.no_grad():
+                for o in (0, 1):
+                    self._tail(o)
+
+    def _issue_select(self, frames, cfg, refresh_shift):
+        """Select on the side stream (in stream order with every earlier
+        select: the spectrum state); recompute counts -> pinned host."""
+        slot = self.k
+        self.k ^= 1
+        main = torch.cuda.current_stream(self.device)
+        st = main if self.select_on_main else self.sel_stream
+        if st is not main:
+            st.wait_stream(main)                 # frames / earlier consumers of this slot
+        with torch.cuda.stream(st):
+            out = self.engine.select(frames, cfg, out=self.outs[slot], refresh_shift=refresh_shift)
+            kf = out.results.view(torch.int32)[:, 6]           # fc_stream_result.k_final
+            rec = self.m.c.tokens - kf                          # recomputed tokens per stream
+            torch.cumsum(rec, 0, out=self.offsets[slot][1:])
+            self.host_counts[slot].copy_(rec, non_blocking=True)
+            self.sel_done[slot].record(st)
+        return slot
 
     @torch.no_grad()
-    def step(self, frames, cfg, refresh_shift=None):
-        """One decision + cached encoder step; returns final hidden states."""
+    def step(self, frames, cfg, refresh_shift=None, next_frames=None):
+        """One decision + cached encoder step; returns final hidden states.
+        ``next_frames``: the next step's frames, whose select is then issued
+        ahead on the side stream (it needs only the frames and this step's
+        spectrum state)."""
         m, B = self.m, self.B
-        out = self.engine.select(frames, cfg, refresh_shift=refresh_shift)
-        rec = out.recompute_idx                       # [B, N] row-major, -1 padded
-        kmax = int((rec >= 0).sum(dim=1).max().item())
-        # pad the recompute batch to a bucket of 128 so GEMM / attention plans
-        # are reused across steps (the -1 rows are masked out)
-        kpad = min(rec.shape[1], max(128, -(-kmax // 128) * 128))
-        rec = rec[:, :kpad]
-        valid = rec >= 0
-        patches = m.patches(frames.to(next(m.parameters()).dtype))
-        p_rec = _gather_rows(patches, rec)
-        x0 = m.embed_tokens(p_rec, rec.clamp_min(0).long())      # [B, K, D]
-        i, o = self.cur, 1 - self.cur
-        if self.mode == "layer1":
-            # layer-0 states of all tokens: reused from the shifted cache, fresh for recomputed
-            splice(out.src_map, self.h0[i], self.ages[i], x0.contiguous(), self.h0[o], self.ages[o],
-                   compact=True)
-            x1 = m.blocks[0].forward_subset(x0, self.h0[o])
-            splice(out.src_map, self.h1[i], self.ages[i], x1.contiguous(), self.h1[o], self.ages[o],
-                   compact=True)
-            x = self.h1[o]
-            for blk in m.blocks[1:]:
-                x = blk(x)
-            y = m.ln(x)
+        if self.pending is not None and self.pending[0] is frames:
+            slot = self.pending[1]
         else:
-            # recomputed tokens of all streams packed stream-major (rec is
-            # front-packed per stream), no padding
-            counts = valid.sum(dim=1)
-            offsets = torch.zeros(B + 1, dtype=torch.int64, device=rec.device)
-            offsets[1:] = torch.cumsum(counts, 0)
-            x = x0[valid]                                   # [sum K_b, D]
-            if x.shape[0] == 0:
-                packed = x0.new_zeros((1, x0.shape[-1]))
+            slot = self._issue_select(frames, cfg, refresh_shift)
+        self.pending = None
+        main = torch.cuda.current_stream(self.device)
+        main.wait_event(self.sel_done[slot])
+        marks = self.debug_marks
+        if marks is not None:
+            marks.append([torch.cuda.Event(enable_timing=True) for _ in range(3)])
+            marks[-1][0].record(main)
+        out = self.outs[slot]
+        if next_frames is not None:
+            self.pending = (next_frames, self._issue_select(next_frames, cfg, refresh_shift))
+        self.sel_done[slot].synchronize()        # the select only, not the encoder queue
+        counts = self.host_counts[slot].tolist()
+        kmax = max(counts)
+        n = m.c.tokens
+        dt = next(m.parameters()).dtype
+        i, o = self.cur, 1 - self.cur
+        # recomputed tokens of all streams packed stream-major without
+        # padding (stream b's k-th recomputed token, row-major, at row
+        # offsets[b] + k — the fc_splice_packed layout); shapes from the host
+        # counts, so nothing here waits on the device
+        total = sum(counts)
+        offsets = self.offsets[slot]
+        if total:
+            sid = torch.repeat_interleave(torch.arange(B, device=self.device), offsets[1:] - offsets[:-1],
+                                          output_size=total)
+            tok = out.recompute_idx[sid, torch.arange(total, device=self.device) - offsets[sid]].long()
+            patches = m.patches(frames.to(dt))
+            x = m.embed(patches[sid, tok]) + m.pos[tok]                     # [T, D] layer-0 states
+        if self.mode == "layer1":
+            blk = m.blocks[0]
+            d = m.c.width
+            # fresh block-0 q | k | v rows of the recomputed tokens, spliced
+            # into the cache of all tokens (reused rows displacement-mapped)
+            qkv = (F.linear(blk.ln1(x), blk.qkv.weight, blk.qkv.bias) if total
+                   else torch.zeros((1, 3 * d), dtype=dt, device=self.device))
+            splice_packed(out.src_map, self.qkv0[i], self.ages[i], qkv, offsets[:B].contiguous(), self.qkv0[o],
+                          self.scratch_ages, status=self.status)
+            if total:
+                # attention over every token of the stream (one dense SDPA);
+                # only the recomputed tokens' rows are kept
+                q, k, v = (blk._heads(t) for t in self.qkv0[o].split(d, dim=-1))
+                att = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).flatten(-2)   # [B, N, D]
+                x = x + blk.proj(att[sid, tok])
+                x1 = x + blk.fc2(F.gelu(blk.fc1(blk.ln2(x)), approximate="tanh"))
             else:
-                seg = torch.unique_consecutive(offsets)     # streams with no recomputed token drop out
-                max_len = int(counts.max().item())
+                x1 = torch.zeros((1, d), dtype=dt, device=self.device)
+            splice_packed(out.src_map, self.h1[i], self.ages[i], x1, offsets[:B].contiguous(), self.h1[o],
+                          self.ages[o], status=self.status)
+            if marks is not None:
+                marks[-1][1].record(main)
+            y = self._tail(o)
+            if marks is not None:
+                marks[-1][2].record(main)
+        else:
+            if total == 0:
+                packed = torch.zeros((1, m.c.width), dtype=dt, device=self.device)
+            else:
+                # segment bounds of the streams that recompute anything (sizes
+                # known on the host, so no device sync)
+                nz = sum(1 for cnt in counts if cnt > 0)
+                keep = torch.nonzero_static(offsets[1:] > offsets[:-1], size=nz).flatten()
+                seg = torch.cat([offsets[:1], offsets[1:][keep]])
                 for blk in m.blocks:
-                    x = blk.forward_packed(x, seg, max_len)
+                    x = blk.forward_packed(x, seg, kmax)
                 packed = m.ln(x)
             splice_packed(out.src_map, self.h1[i], self.ages[i], packed, offsets[:B].contiguous(),
-                          self.h1[o], self.ages[o])
+                          self.h1[o], self.ages[o], status=self.status)
             y = self.h1[o]
         self.cur = o
         return y, out
+
+    def _tail(self, o):
+        """Blocks 1.. and the final LN on every token of cache buffer o —
+        static shapes, so captured once per buffer in a CUDA graph and
+        replayed (no per-kernel host launches)."""
+        m = self.m
+        if self.tail_graphs is None:
+            x = self.h1[o]
+            for blk in m.blocks[1:]:
+                x = blk(x)
+            return m.ln(x)
+        g = self.tail_graphs.get(o)
+        if g is None:
+            st = torch.cuda.Stream(self.device)
+            st.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(st):          # warm-up outside capture (library plans)
+                x = self.h1[o]
+                for blk in m.blocks[1:]:
+                    x = blk(x)
+                m.ln(x)
+            torch.cuda.current_stream(self.device).wait_stream(st)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                x = self.h1[o]
+                for blk in m.blocks[1:]:
+                    x = blk(x)
+                self._tail_out[o] = m.ln(x)
+            self.tail_graphs[o] = g
+        g.replay()
+        return self._tail_out[o]
+
+    def check(self):
+        """Raise AssertionError if a splice met an out-of-bounds source."""
+        from .engine import check_status
+        try:
+            check_status(self.status, "CachedEncoder splice")
+        finally:
+            self.status.zero_()
 
     def flops_per_frame(self, n_tokens):
         """Approximate encoder FLOPs for n tokens (matmuls + attention)."""
         c = self.m.c
         d, f = c.width, c.mlp
-        per_layer = 2 * n * (3 * d * d + d * d + 2 * d * f) + 4 * n * n * d
-        return c.layers * per_layer + 2 * n * 3 * c.patch * c.patch * d
+        per_layer = 2 * n_tokens * (3 * d * d + d * d + 2 * d * f) + 4 * n_tokens * n_tokens * d
+        return c.layers * per_layer + 2 * n_tokens * 3 * c.patch * c.patch * d
+
+
+class GraphedViT:
+    """Full recompute through one CUDA graph (static [B, H, W, 3] input
+    buffer): the baseline the cached step is compared with, launched the same
+    way as the cached step's static tail."""
+
+    def __init__(self, model: ViT, batch: int, device="cuda"):
+        c = model.c
+        self.m = model
+        self.x = torch.zeros((batch, c.image, c.image, 3), dtype=torch.float32, device=device)
+        st = torch.cuda.Stream(device)
+        st.wait_stream(torch.cuda.current_stream(device))
+        with torch.no_grad(), torch.cuda.stream(st):
+            model(self.x)
+        torch.cuda.current_stream(device).wait_stream(st)
+        self.g = torch.cuda.CUDAGraph()
+        with torch.no_grad(), torch.cuda.graph(self.g):
+            self.y = model(self.x)
+
+    def __call__(self, frames):
+        self.x.copy_(frames)
+        self.g.replay()
+        return self.y
 
 
 def cosine(a, b):

@@ -341,6 +341,60 @@ def test_vit_cached_encoder_small(cuda):
                     if s >= 0:
                         assert torch.equal(cache_now[b, p], prev_h[b, s])
             assert float(cosine(y1, model(frames[1])).min()) > 0.5
+            enc.check()
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_vit_layer1_step_matches_reference_semantics(cuda, dtype):
+    """layer1 mode against a plain-torch restatement of its semantics on a
+    small fp32 ViT, with the next step's select issued ahead: for every
+    stream, block-0 queries = recomputed tokens, keys / values = the
+    displacement-mapped cached K/V rows for reused tokens and fresh ones for
+    recomputed tokens; block-0 outputs spliced; blocks 1.. on all tokens."""
+    import torch
+    import torch.nn.functional as F
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    from paper_2604_24391_b200.vit import CachedEncoder, ViT, ViTConfig
+    c = ViTConfig(image=112, patch=14, width=64, mlp=128, heads=2, layers=3)
+    dt = getattr(torch, dtype)   # bf16: the flash-attention varlen path; fp32: per-stream SDPA
+    model = ViT(c).cuda().to(dt).eval()
+    T = 5
+    frames = torch_stream_frames(3, T, 112, 112, seed=9, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    enc = CachedEncoder(model, 3, mode="layer1")
+    blk = model.blocks[0]
+    d = c.width
+    with torch.no_grad():
+        kc = vc = hc = None
+        for t in range(T):
+            y, out = enc.step(frames[t], cfg, next_frames=frames[t + 1] if t + 1 < T else None)
+            x0 = model.embed_tokens(model.patches(frames[t].to(dt)))            # all tokens, layer 0
+            q, k, v = F.linear(blk.ln1(x0), blk.qkv.weight, blk.qkv.bias).split(d, dim=-1)
+            sm = out.src_map.long()
+            if kc is not None:
+                idx = sm.clamp_min(0)[..., None].expand(-1, -1, d)
+                reuse = (sm >= 0)[..., None]
+                k = torch.where(reuse, torch.gather(kc, 1, idx), k)
+                v = torch.where(reuse, torch.gather(vc, 1, idx), v)
+            att = F.scaled_dot_product_attention(blk._heads(q), blk._heads(k), blk._heads(v))
+            x = x0 + blk.proj(att.transpose(1, 2).flatten(-2))
+            h = x + blk.fc2(F.gelu(blk.fc1(blk.ln2(x)), approximate="tanh"))
+            if hc is not None:
+                h = torch.where((sm >= 0)[..., None], torch.gather(hc, 1, sm.clamp_min(0)[..., None].expand(-1, -1, d)), h)
+            kc, vc, hc = k, v, h
+            xr = h
+            for b2 in model.blocks[1:]:
+                xr = b2(xr)
+            ref = model.ln(xr)
+            if dt == torch.float32:
+                assert torch.allclose(y, ref, atol=1e-4, rtol=1e-3), (t, float((y - ref).abs().max()))
+                assert torch.allclose(enc.h1[enc.cur], h, atol=1e-5)
+            else:
+                from paper_2604_24391_b200.vit import cosine
+                assert float(cosine(y, ref).min()) > 0.999, t
+                assert float(cosine(enc.h1[enc.cur], h).min()) > 0.999, t
+        enc.check()
 
 
 def test_inplace_splice_matches_oracle(cuda):
