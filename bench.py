@@ -62,6 +62,8 @@ def parse(argv=None):
     ap.add_argument("--sustained-s", type=float, default=1.5,
                     help="length of the sustained leg (0: skip)")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly")
+    ap.add_argument("--graph-steps", type=int, default=1,
+                    help="pipelined steps per CUDA graph without per-step joins (divides --ring; 1: per-step)")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="whole select per step (no front/back overlap across steps)")
     ap.add_argument("--cpu-streams", type=int, default=64)
@@ -488,9 +490,53 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- one CUDA graph per ring phase (frames[t % R], outs[t & 1] and the
-    # splice ping-pong parity repeat with period R)
-    graphs = None
+    # Chunks of G pipelined steps without per-step joins: the front, back and
+    # splice branches run on their own streams and wait only on the events
+    # of the work they depend on — back(t) on front(t) and on splice(t - 2)
+    # (its output buffer), front(t + 1) on back(t - 1) (its workspace slot),
+    # splice(t - 1) on back(t - 1) — so a branch's tail overlaps the next
+    # step's other branches; the chunk joins once at its end.
+    bs = torch.cuda.Stream(dev)
+    ev = {k: [torch.cuda.Event(), torch.cuda.Event()] for k in ("front", "back", "splice")}
+    live = set()   # (kind, parity) recorded inside the current capture
+
+    def wait(stream, kind, t):
+        if t >= 0 and (kind, t & 1) in live:
+            stream.wait_event(ev[kind][t & 1])
+
+    def mark(stream, kind, t):
+        ev[kind][t & 1].record(stream)
+        live.add((kind, t & 1))
+
+    def chunk(t0, n):
+        cur = torch.cuda.current_stream(dev)
+        live.clear()
+        for st_ in (fs, bs, side):
+            st_.wait_stream(cur)
+        for t in range(t0, t0 + n):
+            wait(fs, "back", t - 1)
+            with torch.cuda.stream(fs):
+                eng.select_front(frames[(t + 1) % R], cfg, outs[(t + 1) & 1], (t + 1) & 1,
+                                 refresh_shift=a.refresh_shift)
+            mark(fs, "front", t + 1)
+            wait(side, "back", t - 1)
+            with torch.cuda.stream(side):
+                spl.step(outs[(t - 1) & 1].src_map, fresh)
+            n_spliced[0] += 1
+            mark(side, "splice", t - 1)
+            wait(bs, "front", t)
+            wait(bs, "splice", t - 2)
+            with torch.cuda.stream(bs):
+                eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=a.refresh_shift)
+            mark(bs, "back", t)
+        for st_ in (fs, bs, side):
+            cur.wait_stream(st_)
+
+    # ---- CUDA graphs: one per ring phase (frames[t % R], outs[t & 1] and
+    # the splice ping-pong parity repeat with period R), and one per chunk
+    # of G phases starting at t = 1 (mod G), G dividing R
+    graphs = chunk_graphs = None
+    G = a.graph_steps if (a.graph_steps > 1 and R % a.graph_steps == 0 and not a.no_pipeline) else 1
     phase(0)                                   # step 0 establishes every stream's spectrum
     t_next = 1
     if not a.no_graph:
@@ -500,26 +546,41 @@ def run_ours(a):
             t = t_next + p
             spl.k = (base + (t - 1)) & 1      # the parity splice(t - 1) has at replay
             graphs.append(StepGraph(lambda t=t: phase(t), device=dev))
+        if G > 1:
+            chunk_graphs = []
+            for c0 in range(1, R + 1, G):
+                spl.k = (base + (c0 - 1)) & 1
+                chunk_graphs.append(StepGraph(lambda c0=c0: chunk(c0, G), device=dev))
         n_spliced[0] = base
         spl.k = base & 1
         torch.cuda.synchronize()
 
-    def run(t):
-        if graphs is None:
-            phase(t)
-        else:
-            graphs[(t - 1) % R].replay()
-            n_spliced[0] += 1
-            spl.k = n_spliced[0] & 1
-        launches[0] += per_phase
+    def advance(n):
+        """n pipelined steps from t_next (whole chunks where aligned)."""
+        nonlocal t_next
+        while n > 0:
+            t = t_next
+            if chunk_graphs is not None and (t - 1) % G == 0 and n >= G:
+                chunk_graphs[((t - 1) % R) // G].replay()
+                k = G
+            elif graphs is not None:
+                graphs[(t - 1) % R].replay()
+                k = 1
+            else:
+                phase(t)
+                k = 1
+            if graphs is not None:
+                n_spliced[0] += k
+                spl.k = n_spliced[0] & 1
+            launches[0] += per_phase * k
+            t_next += k
+            n -= k
 
     # clock sampling starts before the warm-up, so the GPU does not idle while
     # nvidia-smi starts; only samples inside the timed region are kept
     clocks = ClockSampler(local).__enter__()
     # ---- warm-up: step 0 (above) + W - 1 pipelined steps
-    for _ in range(max(0, a.warmup - 1)):
-        run(t_next)
-        t_next += 1
+    advance(max(0, a.warmup - 1))
     barrier()
 
     # ---- timed region: K pipelined steps (K selects beside K splices), CUDA
@@ -533,9 +594,7 @@ def run_ours(a):
         barrier()
         clocks.start()
         ev0.record(stream)
-        for _ in range(a.steps):
-            run(t_next)
-            t_next += 1
+        advance(a.steps)
         ev1.record(stream)
         barrier()
         win_main = clocks.stop()
@@ -551,9 +610,7 @@ def run_ours(a):
             barrier()
             clocks.start()
             s0.record(stream)
-            for _ in range(n_s):
-                run(t_next)
-                t_next += 1
+            advance(n_s)
             s1.record(stream)
             barrier()
             win_s = clocks.stop()
@@ -779,6 +836,7 @@ def run_ours(a):
             "config": {"workload": (f"config5 {'weak: ' + str(a.streams) + ' streams per GPU' if a.weak else 'as written: ' + str(total_streams) + ' streams in total, ' + str(S) + ' per GPU'}"
                                     ": select + splice, adaptive budget, refresh on shift>1"),
                        "graph": not a.no_graph, "pipeline": not a.no_pipeline,
+                       "graph_steps": G if not a.no_graph else 0,
                        "streams_per_gpu": S, "streams_total": total_streams, "size": H, "channels": 3, "patch": P, "tokens": N,
                        "hidden": D, "hidden_dtype": "bf16", "frame_ring_steps": R,
                        "l2": f"inputs > L2 ({S * H * H * 12 / 1e9:.2f} GB of frames per step, "

@@ -17,6 +17,7 @@ float64 gray frame.
 
 from __future__ import annotations
 
+import re
 import struct
 from pathlib import Path
 
@@ -28,161 +29,169 @@ RAWF32_MAGIC = b"FQC1"          # frameio.py:21
 RAWF32_HEADER = 16              # frameio.py:22
 LUMA_WEIGHTS = (0.299, 0.587, 0.114)   # frameio.py:26
 
+# Netpbm header grammar (frameio.py:29-50): fields are runs of non-blank
+# bytes; blanks and `#` comments (to end of line) separate them; exactly one
+# blank byte ends the header after maxval.
+_BLANKS = b" \t\n\r\x0b\x0c"
+_GAP = re.compile(rb"(?:[ \t\n\r\x0b\x0c]|#[^\n\r]*)*")
+_FIELD = re.compile(rb"[^ \t\n\r\x0b\x0c]+")
+_CHANNELS = {b"P5": 1, b"P6": 3}
 
-def _tokenize_netpbm(data, count, path):
-    """Header tokens and the payload offset (frameio.py:29-50): tokens are
-    whitespace-delimited, ``#`` starts a comment that runs to end of line, and
-    exactly one whitespace byte separates maxval from the payload."""
-    tokens = []
-    pos, n = 0, len(data)
-    while len(tokens) < count:
-        if pos >= n:
-            raise FrameParseError(f"{path}: truncated header", offset=pos)
-        c = data[pos:pos + 1]
-        if c.isspace():
-            pos += 1
-        elif c == b"#":
-            while pos < n and data[pos:pos + 1] not in (b"\n", b"\r"):
-                pos += 1
-        else:
-            start = pos
-            while pos < n and not data[pos:pos + 1].isspace():
-                pos += 1
-            tokens.append(data[start:pos])
-    if pos >= n:
-        raise FrameParseError(f"{path}: missing pixel data", offset=pos)
-    return tokens, pos + 1
+
+class _Fail(Exception):
+    """A parse failure before the file name is attached: (message, offset)."""
+
+
+def _header_fields(data, want):
+    """The first ``want`` header fields and the payload offset."""
+    fields, at, end = [], 0, len(data)
+    for _ in range(want):
+        at = _GAP.match(data, at).end()
+        if at >= end:
+            raise _Fail("truncated header", at)
+        m = _FIELD.match(data, at)
+        fields.append(m.group())
+        at = m.end()
+    if at >= end:
+        raise _Fail("missing pixel data", at)
+    return fields, at + 1
+
+
+def _netpbm(data):
+    """(uint8 pixels (H, W) or (H, W, 3), channels) of P5 / P6 bytes."""
+    if len(data) < 2:
+        raise _Fail("file too short", len(data))
+    channels = _CHANNELS.get(data[:2])
+    if channels is None:
+        raise _Fail(f"unsupported magic {data[:2]!r}", 0)
+    fields, at = _header_fields(data, 4)
+    try:
+        width, height, maxval = map(int, fields[1:])
+    except ValueError:
+        raise _Fail("non-numeric header field", 2) from None
+    rules = ((width >= 1 and height >= 1, f"invalid dimensions {width}x{height}"),
+             (maxval == 255, f"only maxval 255 supported, got {maxval}"))
+    for ok, msg in rules:
+        if not ok:
+            raise _Fail(msg, 2)
+    count = width * height * channels
+    body = memoryview(data)[at:at + count]
+    if body.nbytes < count:
+        raise _Fail(f"truncated pixel data, expected {count} bytes", at + body.nbytes)
+    px = np.frombuffer(body, dtype=np.uint8)
+    return px.reshape((height, width) if channels == 1 else (height, width, 3)), channels
+
+
+def _parse(path, parser):
+    path = Path(path)
+    try:
+        return parser(path.read_bytes())
+    except _Fail as f:
+        msg, offset = f.args
+        raise FrameParseError(f"{path}: {msg}", offset=offset) from None
 
 
 def read_netpbm_payload(path):
     """Parse a P5 / P6 file (frameio.py:53-80): returns (uint8 pixels of
     shape (H, W) or (H, W, 3), channels)."""
-    path = Path(path)
-    data = path.read_bytes()
-    if len(data) < 2:
-        raise FrameParseError(f"{path}: file too short", offset=len(data))
-    magic = data[:2]
-    if magic not in (b"P5", b"P6"):
-        raise FrameParseError(f"{path}: unsupported magic {magic!r}", offset=0)
-    tokens, at = _tokenize_netpbm(data, 4, path)
-    try:
-        width, height, maxval = (int(t) for t in tokens[1:])
-    except ValueError:
-        raise FrameParseError(f"{path}: non-numeric header field", offset=2)
-    if width < 1 or height < 1:
-        raise FrameParseError(f"{path}: invalid dimensions {width}x{height}", offset=2)
-    if maxval != 255:
-        raise FrameParseError(f"{path}: only maxval 255 supported, got {maxval}", offset=2)
-    channels = 1 if magic == b"P5" else 3
-    need = width * height * channels
-    payload = data[at:at + need]
-    if len(payload) < need:
-        raise FrameParseError(f"{path}: truncated pixel data, expected {need} bytes",
-                              offset=at + len(payload))
-    px = np.frombuffer(payload, dtype=np.uint8)
-    shape = (height, width) if channels == 1 else (height, width, 3)
-    return px.reshape(shape), channels
+    return _parse(path, _netpbm)
 
 
 def read_netpbm(path):
     """P5 gray / P6 luma-reduced frame as float64 in [0, 1] (frameio.py:53-88)."""
     px, channels = read_netpbm_payload(path)
-    p = px.astype(np.float64)
-    if channels == 1:
-        gray = p
-    else:
-        gray = LUMA_WEIGHTS[0] * p[..., 0] + LUMA_WEIGHTS[1] * p[..., 1] + LUMA_WEIGHTS[2] * p[..., 2]
-    return gray / 255.0
+    v = px.astype(np.float64)
+    if channels == 3:
+        # left-to-right sum, as the reference writes it
+        v = (LUMA_WEIGHTS[0] * v[..., 0] + LUMA_WEIGHTS[1] * v[..., 1]) + LUMA_WEIGHTS[2] * v[..., 2]
+    return v / 255.0
+
+
+def _u8_image(values):
+    a = np.asarray(values)
+    if a.ndim != 2:
+        raise ValueError(f"image must be 2D, got shape {a.shape}")
+    return a if a.dtype == np.uint8 else np.round(np.clip(a, 0.0, 1.0) * 255.0).astype(np.uint8)
 
 
 def write_pgm(path, values):
     """Binary P5, maxval 255; float data clipped to [0, 1] and quantised
     (frameio.py:91-105)."""
-    arr = np.asarray(values)
-    if arr.ndim != 2:
-        raise ValueError(f"image must be 2D, got shape {arr.shape}")
-    if arr.dtype != np.uint8:
-        arr = np.round(np.clip(arr, 0.0, 1.0) * 255.0).astype(np.uint8)
-    h, w = arr.shape
-    with open(path, "wb") as fh:
-        fh.write(f"P5\n{w} {h}\n255\n".encode("ascii"))
-        fh.write(arr.tobytes())
+    img = _u8_image(values)
+    header = b"P5\n%d %d\n255\n" % (img.shape[1], img.shape[0])
+    Path(path).write_bytes(header + img.tobytes())
 
 
-def _validate(f):
+def _finite_2d(f):
     a = np.asarray(f, dtype=np.float64)
-    if a.ndim != 2:
-        raise ValueError(f"frame must be 2D, got shape {a.shape}")
-    if a.shape[0] < 1 or a.shape[1] < 1:
-        raise ValueError(f"frame dimensions must be >= 1, got {a.shape}")
-    if not np.all(np.isfinite(a)):
-        raise ValueError("frame contains non-finite values")
+    problem = ("frame must be 2D, got shape %s" % (a.shape,) if a.ndim != 2 else
+               "frame dimensions must be >= 1, got %s" % (a.shape,) if min(a.shape) < 1 else
+               "frame contains non-finite values" if not np.isfinite(a).all() else None)
+    if problem:
+        raise ValueError(problem)
     return a
 
 
 def save_rawf32(path, frames):
     """rawf32 container writer (frameio.py:107-115)."""
-    stack = np.stack([_validate(f) for f in frames]).astype("<f4")
+    stack = np.stack([_finite_2d(f) for f in frames]).astype("<f4")
     t, h, w = stack.shape
-    with open(path, "wb") as fh:
-        fh.write(RAWF32_MAGIC)
-        fh.write(struct.pack("<III", h, w, t))
-        fh.write(stack.tobytes())
+    Path(path).write_bytes(RAWF32_MAGIC + struct.pack("<III", h, w, t) + stack.tobytes())
+
+
+def _rawf32(data):
+    """float32 [T, H, W] view of rawf32 bytes (frameio.py:118-139)."""
+    if len(data) < RAWF32_HEADER:
+        raise _Fail("truncated rawf32 header", len(data))
+    if data[:4] != RAWF32_MAGIC:
+        raise _Fail(f"bad magic {data[:4]!r}, expected {RAWF32_MAGIC!r}", 0)
+    h, w, t = struct.unpack_from("<III", data, 4)
+    if min(h, w, t) < 1:
+        raise _Fail(f"invalid header dimensions {h}x{w}x{t}", 4)
+    size = RAWF32_HEADER + 4 * h * w * t
+    if len(data) != size:
+        raise (_Fail(f"truncated rawf32 payload, expected {size} bytes", len(data)) if len(data) < size
+               else _Fail("trailing bytes after payload", size))
+    return np.frombuffer(data, dtype="<f4", count=h * w * t, offset=RAWF32_HEADER).reshape(t, h, w)
 
 
 def _rawf32_payload(path):
-    """Header checks of frameio.py:118-139; returns float32 [T, H, W]."""
-    path = Path(path)
-    data = path.read_bytes()
-    if len(data) < RAWF32_HEADER:
-        raise FrameParseError(f"{path}: truncated rawf32 header", offset=len(data))
-    if data[:4] != RAWF32_MAGIC:
-        raise FrameParseError(f"{path}: bad magic {data[:4]!r}, expected {RAWF32_MAGIC!r}", offset=0)
-    h, w, t = struct.unpack("<III", data[4:16])
-    if h < 1 or w < 1 or t < 1:
-        raise FrameParseError(f"{path}: invalid header dimensions {h}x{w}x{t}", offset=4)
-    need = RAWF32_HEADER + 4 * h * w * t
-    if len(data) < need:
-        raise FrameParseError(f"{path}: truncated rawf32 payload, expected {need} bytes", offset=len(data))
-    if len(data) > need:
-        raise FrameParseError(f"{path}: trailing bytes after payload", offset=need)
-    return np.frombuffer(data, dtype="<f4", count=h * w * t, offset=RAWF32_HEADER).reshape(t, h, w), path
+    return _parse(path, _rawf32), Path(path)
 
 
 def load_rawf32(path):
     """rawf32 reader (frameio.py:118-146): float64 frames, non-finite rejected."""
     vals, path = _rawf32_payload(path)
-    frames = vals.astype(np.float64)
-    for t in range(frames.shape[0]):
-        if not np.all(np.isfinite(frames[t])):
-            raise FrameParseError(f"{path}: frame {t} contains non-finite values")
-    return [frames[t] for t in range(frames.shape[0])]
+    bad = np.flatnonzero(~np.isfinite(vals).reshape(vals.shape[0], -1).all(axis=1))
+    if bad.size:
+        raise FrameParseError(f"{path}: frame {int(bad[0])} contains non-finite values")
+    return list(vals.astype(np.float64))
+
+
+_NETPBM_SUFFIXES = (".pgm", ".ppm")
 
 
 def _resolve(path, fmt):
+    """(format, files) of a rawf32 file, a netpbm file or a directory of
+    netpbm files in sorted order."""
     path = Path(path)
     if fmt == "auto":
-        if path.is_dir() or path.suffix.lower() in (".pgm", ".ppm"):
-            fmt = "pgm"
-        else:
-            fmt = "rawf32"
+        fmt = "pgm" if (path.is_dir() or path.suffix.lower() in _NETPBM_SUFFIXES) else "rawf32"
     if fmt not in ("rawf32", "pgm"):
         raise ValueError(f"unknown format {fmt!r}")
-    if fmt == "pgm" and path.is_dir():
-        files = sorted(p for p in path.iterdir() if p.suffix.lower() in (".pgm", ".ppm"))
-        if not files:
-            raise FrameParseError(f"{path}: no .pgm/.ppm files found")
-        return fmt, files
-    return fmt, [path]
+    if fmt == "rawf32" or not path.is_dir():
+        return fmt, [path]
+    files = sorted(p for p in path.iterdir() if p.suffix.lower() in _NETPBM_SUFFIXES)
+    if not files:
+        raise FrameParseError(f"{path}: no .pgm/.ppm files found")
+    return fmt, files
 
 
 def load_frames(path, fmt="auto"):
     """Ordered frame list from a rawf32 file, a netpbm file or a directory of
     them in sorted order (frameio.py:149-175)."""
     fmt, files = _resolve(path, fmt)
-    if fmt == "rawf32":
-        return load_rawf32(files[0])
-    return [read_netpbm(p) for p in files]
+    return load_rawf32(files[0]) if fmt == "rawf32" else list(map(read_netpbm, files))
 
 
 def load_frames_device(path, fmt="auto", device=None):
@@ -232,6 +241,7 @@ def export_energy_heatmap(energy_map, path):
     """Per-patch energy map as an 8-bit PGM, hottest patch = 255
     (frameio.py:178-188)."""
     e = np.asarray(energy_map.energies, dtype=np.float64)
-    peak = float(e.max())
-    write_pgm(path, e / peak if peak > 0.0 else np.zeros_like(e))
+    top = float(e.max())
+    scaled = np.zeros_like(e) if top <= 0.0 else e / top
+    write_pgm(path, scaled)
     return Path(path)

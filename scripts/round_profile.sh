@@ -14,9 +14,9 @@ timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 cat gpurun_out/bench_$TAG.json
 KRE="k448|k_select|k_rank|k_splice"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$KRE" --csv \
-    --log-file gpurun_out/launches_$TAG.csv python bench.py --no-cpu-baseline > /dev/null 2>&1
+    --log-file gpurun_out/launches_$TAG.csv python bench.py --no-cpu-baseline --sustained-s 0 > /dev/null 2>&1
 echo launches_rc=$?
-CMD="python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline"
+CMD="python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline --sustained-s 0"
 timeout 600 $CMD > /dev/null 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on \
     -k regex:"k448_rows_fwd|k448_cols|k448_rows_inv|k_select|k_rank|k_splice_ip|k_splice_plan" -s 14 -c 7 \
     -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
