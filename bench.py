@@ -655,7 +655,7 @@ def run_ours(a):
     spec = 8 * H * ((H // 2 + 7) // 8) * 8   # one packed half-spectrum, fp32 complex
     kbytes = [
         S * (12 * hw + spec + 8 * N),          # rows_fwd K_A: RGB in, packed rows (T1) out, energies
-        S * (4 * spec),                        # cols K_B: T1 in, state in/out, T2 out
+        S * ((3 if kms[2] == 0 else 4) * spec),  # cols K_B: T1 in, state in/out, T2 out (K_BC fused: no T2)
         S * spec,                              # rows_inv K_C: T2 in
         S * (3 * N + 14 * N + 136),            # select K_D: order + refresh mask in, masks/indices out
         S * (8 * N + 3 * N + 32),              # rank K_D1: energies in, order + refresh mask + stats out
@@ -680,8 +680,9 @@ def run_ours(a):
                      "note": "SURVEY 8(d) algorithmic bytes; the in-place splice moves only recomputed "
                              "rows of zero-displacement streams: frac_moved counts the select bytes plus "
                              "the splice bytes actually moved"}
+    # (a kind with no launch, e.g. rows_inv when K_B + K_C run fused, is left out)
     kernels = {names[k]: {"ms": kms[k], "share": kms[k] / sum(kms), "bytes": kbytes[k],
-                          "gbs": kbytes[k] / (kms[k] / 1e3) / 1e9} for k in range(nk)}
+                          "gbs": kbytes[k] / (kms[k] / 1e3) / 1e9} for k in range(nk) if kms[k] > 0}
     # ncu DRAM bytes per launch of the same kernel, from the capture named in
     # profiles/traffic.json (tagged with its capture id: it is not re-measured
     # by this run)

@@ -21,6 +21,7 @@
 
 #include "fc_kernels.cuh"
 #include "fc_fast448w.cuh"
+#include "fc_fast448c.cuh"
 #include "fc_compare.cuh"
 #include "fc_stages.cuh"
 #include "fc_spectral.cuh"
@@ -57,6 +58,7 @@ struct fc_plan {
   void* fnB = nullptr;                 // K_B / K_C variants (occupancy x twiddle mode)
   bool t2_tma = false;                 // K_B stores T2 with a TMA tensor store
   bool t1_tma = false;                 // K_A stores T1 with a TMA tensor store
+  bool fused_bc = false;               // K_B + K_C as one cluster kernel (T2 through DSMEM)
   void* fnC = nullptr;
   float2* d_twW = nullptr;
   float2* d_twH = nullptr;
@@ -321,7 +323,10 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
         if (rec) rec->mark(st, 0);
         launch_rank(pl, cfg, kp, b0, nb, ls, part == kAll && !rec, rec);
       }
-      if (back) {
+      if (back && pl->fused_bc) {
+        k448_colsinv<true><<<dim3(kClusterBC, nb), 32 * kWarpsBC, kSmemBC, ls>>>(kl, b0);
+        if (rec) rec->mark(st, 1);
+      } else if (back) {
         auto fb = (void (*)(KParams, int, CUtensorMap))pl->fnB;
         fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm2[l]);
         if (rec) rec->mark(st, 1);
@@ -438,8 +443,11 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     pl->smemA = (size_t)kPxBytes448;
     pl->smemB = (size_t)kSmemB448;
     pl->smemC = (size_t)kSmemC448;
-    kp.NCB = kNCB448;   // K_B stats partials per stream
-    kp.NRG = kNRG448;   // K_C peak partials per stream
+    // K_B / K_C, or the fused cluster kernel K_BC (FC_FUSED_BC=1), whose
+    // partials are one per column / one per warp
+    pl->fused_bc = env_int("FC_FUSED_BC", 0, 0, 1) != 0;
+    kp.NCB = pl->fused_bc ? kNCBf : kNCB448;   // stats partials per stream
+    kp.NRG = pl->fused_bc ? kNRGf : kNRG448;   // peak partials per stream
     // [T1 slot 0: lanes x chunk streams | T1 slot 1 | T2], lanes contiguous
     // inside each, so a launch over the whole batch can also address them
     pl->lane_t1 = (size_t)pl->chunk * 224 * 448 * sizeof(float2);
@@ -552,6 +560,7 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
               : oc == 7 ? (void*)k448_rows_inv<7, true> : (void*)k448_rows_inv<6, false>;
       if (rc == FC_OK) rc = set_smem(pl->fnB, pl->smemB);
       if (rc == FC_OK) rc = set_smem(pl->fnC, pl->smemC);
+      if (rc == FC_OK && pl->fused_bc) rc = set_smem((void*)k448_colsinv<true>, kSmemBC);
     } else {
       rc = set_smem(sel_rows_fwd(pl->kw), pl->smemA);
       if (rc == FC_OK) rc = set_smem(sel_cols(pl->kh), pl->smemB);
@@ -601,8 +610,8 @@ int64_t fc_plan_workspace_bytes(const fc_plan* pl) { return pl ? (int64_t)pl->ws
 int fc_plan_tokens(const fc_plan* pl) { return pl ? pl->kp.N : -1; }
 int fc_plan_launches(const fc_plan* pl) {
   if (!pl) return -1;
-  // fast: K_A, K_D1, K_B, K_C per chunk + K_D; generic: the five kernels once
-  return pl->fast ? 4 * ((pl->g.batch + pl->chunk - 1) / pl->chunk) + 1 : 5;
+  // fast: K_A, K_D1, K_B, K_C (or K_BC) per chunk + K_D; generic: the five kernels once
+  return pl->fast ? (pl->fused_bc ? 3 : 4) * ((pl->g.batch + pl->chunk - 1) / pl->chunk) + 1 : 5;
 }
 
 int fc_state_reset(const fc_plan* pl, void* state, int32_t first, int32_t count, void* stream) {

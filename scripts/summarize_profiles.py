@@ -21,7 +21,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 OUT = ROOT / "gpurun_out"
 PROF = ROOT / "profiles"
-NAMES = {"k448_rows_fwd": "rows_fwd", "k448_cols": "cols", "k448_rows_inv": "rows_inv",
+NAMES = {"k448_rows_fwd": "rows_fwd", "k448_cols": "cols", "k448_rows_inv": "rows_inv", "k448_colsinv": "cols",
          "k_select": "select", "k_rank": "rank", "k_splice16": "splice", "k_splice_ip": "splice", "k_splice_ip_bulk": "splice",
          "k_splice_plan": "splice_plan"}
 

@@ -504,3 +504,47 @@ def test_split_phase_pipeline_bit_identical(cuda, size, streams):
             assert torch.equal(getattr(o, name), getattr(r, name)), (t, name)
         cur.wait_stream(fs)
     assert torch.equal(pip.state, ref.state)
+
+
+@pytest.mark.parametrize("streams", [40, 3])
+def test_fused_cluster_colsinv_matches_split_kernels(cuda, monkeypatch, streams):
+    """K_BC (FC_FUSED_BC=1: K_B + K_C in one 8-CTA cluster per stream, the
+    cross-power handed over through distributed shared memory) computes the
+    same transforms as K_B -> T2 -> K_C: identical decisions, splice maps,
+    energies and spectrum state; sim / entropy within fp64 rounding of a
+    different partial-sum grouping; and the oracle agrees."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.api import decision_from_device
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    T = 4
+    frames = torch_stream_frames(streams, T, 448, 448, seed=31, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    monkeypatch.setenv("FC_FUSED_BC", "0")
+    split = fc.FreqCacheEngine(streams, 448, 448, 14, fmt="rgb")
+    monkeypatch.setenv("FC_FUSED_BC", "1")
+    fused = fc.FreqCacheEngine(streams, 448, 448, 14, fmt="rgb")
+    oc = O.OracleConfig(patch_size=14, refresh_shift=1)
+    rep = ParityReport()
+    for t in range(T):
+        a = split.select(frames[t], cfg, refresh_shift=1)
+        b = fused.select(frames[t], cfg, refresh_shift=1)
+        for name in ("reuse_idx", "recompute_idx", "src_map", "reuse_mask", "refresh_mask", "energy"):
+            assert torch.equal(getattr(a, name), getattr(b, name)), (t, name)
+        ra, rb = a.host_results(), b.host_results()
+        for f in ("status", "cold", "flushed", "diagnostic", "k_reuse", "k_candidate", "k_final", "di", "dj",
+                  "di_patches", "dj_patches", "n_refresh"):
+            assert np.array_equal(ra[f], rb[f]), (t, f)
+        for f in ("peak", "peak_runner_up"):
+            assert np.array_equal(ra[f], rb[f]), (t, f)   # same transforms, same argmax
+        for f in ("sim_freq", "entropy_raw", "entropy_norm", "alpha"):
+            assert np.allclose(ra[f], rb[f], rtol=1e-12, atol=0), (t, f)
+        if t:
+            fr = frames.cpu().numpy()
+            for s in (0, streams - 1):
+                d = decision_from_device(rb[s], b.reuse_idx[s].cpu().numpy(), b.recompute_idx[s].cpu().numpy(),
+                                         b.refresh_mask[s].cpu().numpy(), step=t)
+                compare(d, O.decide(fr[t - 1, s], fr[t, s], oc, step=t), oc, energies=b.energy[s].cpu().numpy(),
+                        rep=rep)
+    assert torch.equal(split.state, fused.state)
+    assert rep.ok, rep.errors
