@@ -271,6 +271,14 @@ int  fc_compare_cosines(const fc_geometry* geom, const void* prev, const void* c
 int  fc_row_cosines(int64_t n, int64_t d, const double* a, const double* b,
                     double* out, void* cuda_stream);
 
+/* ---- encoder-side token gather (BASELINE config 4).  Row r of out (bf16,
+ * [rows][3 P^2], (py, px, channel) order) = the P x P patch of token
+ * index[r] = b * N + p of the fp32 RGB frames [batch][H][W][3]: the pixels
+ * of the recomputed tokens only, as a ViT patch embedding consumes them.   */
+int  fc_gather_patches(int32_t rows, int32_t batch, int32_t height, int32_t width,
+                       int32_t patch_size, const float* frames, const int64_t* index,
+                       void* out_bf16, void* cuda_stream);
+
 /* ---- fp64 transform wrappers (spectral.py:24-72, migration.py:128-134):
  * the reference's public transform API, on the GPU in fp64 (dense passes
  * with exact twiddles; not the decision path's packed fp32 FFTs).  Complex

@@ -48,7 +48,7 @@ EXPORTS = (
     "fc_splice_inplace", "fc_splice_inplace_scratch_bytes", "fc_compare_cosines", "fc_row_cosines",
     "fc_graph_capture_begin", "fc_graph_capture_end", "fc_graph_launch", "fc_graph_destroy",
     "fc_dft2_workspace_bytes", "fc_dft2", "fc_phase_correlation_workspace_bytes", "fc_phase_correlation_spectra",
-    "fc_block_dct", "fc_amplitude_phase",
+    "fc_block_dct", "fc_amplitude_phase", "fc_gather_patches",
 )
 
 
@@ -141,6 +141,7 @@ def load(path=None):
         "fc_phase_correlation_spectra": (C.c_int, [i32, i32, vp, vp, vp, vp, vp]),
         "fc_block_dct": (C.c_int, [i32, i32, vp, vp, vp]),
         "fc_amplitude_phase": (C.c_int, [i64, vp, vp, vp, vp]),
+        "fc_gather_patches": (C.c_int, [i32, i32, i32, i32, i32, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

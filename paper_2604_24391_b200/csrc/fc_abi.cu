@@ -12,6 +12,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 
 #include <cmath>
 #include <cstdlib>
@@ -1011,6 +1012,42 @@ int fc_graph_launch(void* exec, void* stream) {
 
 void fc_graph_destroy(void* exec) {
   if (exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
+}
+
+// ------------------------------------------------------ patch gather ----
+// Recomputed tokens' pixels for an encoder (BASELINE config 4): packed row r
+// of `out` is the P x P x 3 patch of token index[r] = b * N + p, read straight
+// from the fp32 RGB frames and written as bf16 in (py, px, channel) order —
+// the layout of a ViT patch embedding's input.  One warp per row; only the
+// recomputed tokens' pixels are read.
+namespace {
+__global__ void k_gather_patches(int rows, int H, int W, int P, const float* __restrict__ frames,
+                                 const int64_t* __restrict__ index, __nv_bfloat16* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int cols = W / P, n = (H / P) * cols, per = 3 * P * P;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+    const int64_t t = index[r];
+    const int b = (int)(t / n), p = (int)(t - (int64_t)b * n);
+    const int i = p / cols, j = p - (p / cols) * cols;
+    const float* base = frames + (((size_t)b * H + (size_t)i * P) * W + (size_t)j * P) * 3;
+    __nv_bfloat16* o = out + (size_t)r * per;
+    for (int e = lane; e < per; e += 32) {
+      const int py = e / (3 * P), rem = e - py * 3 * P;   // rem = px * 3 + channel
+      o[e] = __float2bfloat16_rn(base[(size_t)py * W * 3 + rem]);
+    }
+  }
+}
+}  // namespace
+
+int fc_gather_patches(int32_t rows, int32_t batch, int32_t height, int32_t width, int32_t patch_size,
+                      const float* frames, const int64_t* index, void* out_bf16, void* stream) {
+  if (rows < 0 || batch < 1 || patch_size < 1 || height % patch_size || width % patch_size) return FC_EINVAL;
+  if (rows == 0) return FC_OK;
+  if (!frames || !index || !out_bf16) return FC_EINVAL;
+  const int blocks = (int)(((int64_t)rows * 32 + 255) / 256 < 8192 ? ((int64_t)rows * 32 + 255) / 256 : 8192);
+  k_gather_patches<<<blocks, 256, 0, as_stream(stream)>>>(rows, height, width, patch_size, frames, index,
+                                                         reinterpret_cast<__nv_bfloat16*>(out_bf16));
+  return launch_check();
 }
 
 // --------------------------------------------------------- mask images ----

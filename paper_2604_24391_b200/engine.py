@@ -251,6 +251,25 @@ def compare_cosines(prev, curr, patch_size, visual=None, naive=None):
     return visual, naive
 
 
+def gather_patches(frames, patch_size, index, out=None):
+    """bf16 [T, 3 P^2] pixels of the tokens ``index`` (int64 [T], b * N + p)
+    of fp32 RGB frames [B, H, W, 3], in a ViT patch embedding's (py, px, c)
+    order (``fc_gather_patches``)."""
+    lib = nat.lib()
+    if frames.dtype != torch.float32 or frames.dim() != 4 or frames.shape[-1] != 3 or not frames.is_contiguous():
+        raise ValueError("frames must be a contiguous float32 [B, H, W, 3] tensor")
+    if index.dtype != torch.int64 or index.dim() != 1 or not index.is_contiguous():
+        raise ValueError("index must be a contiguous int64 [T] tensor")
+    B, H, W, _ = (int(v) for v in frames.shape)
+    p = int(patch_size)
+    if out is None:
+        out = torch.empty((index.numel(), 3 * p * p), dtype=torch.bfloat16, device=frames.device)
+    rc = lib.fc_gather_patches(int(index.numel()), B, H, W, p, _ptr(frames), _ptr(index), _ptr(out),
+                               _stream(frames.device))
+    nat.check(rc, "fc_gather_patches")
+    return out
+
+
 def row_cosines(a, b, out=None):
     """Row-wise cosine of two [n, d] float64 device stacks (compare.py:28-38)."""
     lib = nat.lib()

@@ -36,7 +36,7 @@ from dataclasses import dataclass
 import torch
 import torch.nn.functional as F
 
-from .engine import FreqCacheEngine, splice, splice_packed
+from .engine import FreqCacheEngine, gather_patches, splice, splice_packed
 
 try:  # variable-length attention for the packed subset mode (library kernel)
     from flash_attn import flash_attn_varlen_func as _flash_varlen
@@ -192,6 +192,18 @@ class CachedEncoder:
             self.qkv0 = torch.zeros((2, batch, n, 3 * d), dtype=dt, device=device)
         self.tail_graphs = {} if (graphs and mode == "layer1") else None
         self._tail_out = {}
+        # layer1 with graphs: the packed block-0 work of a step is replayed
+        # from a CUDA graph per (row bucket, cache buffer); its per-step inputs
+        # are copied into static buffers first
+        self.b0_graphs = {} if self.tail_graphs is not None else None
+        nb = batch * n
+        self.bucket = max(64, min(1024, -(-nb // 16 // 64) * 64))   # ~16 row buckets
+        if self.b0_graphs is not None:
+            self.st_frames = torch.zeros((batch, c.image, c.image, 3), dtype=torch.float32, device=device)
+            self.st_src = torch.zeros((batch, n), dtype=torch.int32, device=device)
+            self.st_rec = torch.zeros((batch, n), dtype=torch.int32, device=device)
+            self.st_offsets = torch.zeros(batch + 1, dtype=torch.int64, device=device)
+            self._pool = torch.cuda.graph_pool_handle()
         self.ages = torch.zeros((2, batch, n), dtype=torch.int64, device=device)
         self.scratch_ages = torch.zeros((batch, n), dtype=torch.int64, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)      # splice bounds flag
@@ -208,10 +220,11 @@ class CachedEncoder:
         self.sel_done = [torch.cuda.Event(), torch.cuda.Event()]
         self.pending = None   # (frames tensor, slot) of a select issued ahead
         self.k = 0
-        if self.tail_graphs is not None:   # capture both tail graphs up front
+        if self.tail_graphs is not None:   # capture every graph up front (fresh, all-zero caches)
             with torch.no_grad():
                 for o in (0, 1):
                     self._tail(o)
+            self.prepare_graphs()
 
     def _issue_select(self, frames, cfg, refresh_shift):
         """Select on the side stream (in stream order with every earlier
@@ -250,8 +263,6 @@ class CachedEncoder:
             marks.append([torch.cuda.Event(enable_timing=True) for _ in range(3)])
             marks[-1][0].record(main)
         out = self.outs[slot]
-        if next_frames is not None:
-            self.pending = (next_frames, self._issue_select(next_frames, cfg, refresh_shift))
         self.sel_done[slot].synchronize()        # the select only, not the encoder queue
         counts = self.host_counts[slot].tolist()
         kmax = max(counts)
@@ -264,12 +275,28 @@ class CachedEncoder:
         # counts, so nothing here waits on the device
         total = sum(counts)
         offsets = self.offsets[slot]
+        if self.mode == "layer1" and self.b0_graphs is not None and total:
+            self.st_frames.copy_(frames)
+            self.st_src.copy_(out.src_map)
+            self.st_rec.copy_(out.recompute_idx)
+            self.st_offsets.copy_(offsets)
+            tp = -(-total // self.bucket) * self.bucket
+            self._block0_graph(tp, o).replay()
+            self._prefetch(next_frames, cfg, refresh_shift)
+            if marks is not None:
+                marks[-1][1].record(main)
+            y = self._tail(o)
+            if marks is not None:
+                marks[-1][2].record(main)
+            self.cur = o
+            return y, out
         if total:
             sid = torch.repeat_interleave(torch.arange(B, device=self.device), offsets[1:] - offsets[:-1],
                                           output_size=total)
-            tok = out.recompute_idx[sid, torch.arange(total, device=self.device) - offsets[sid]].long()
-            patches = m.patches(frames.to(dt))
-            x = m.embed(patches[sid, tok]) + m.pos[tok]                     # [T, D] layer-0 states
+            pos = torch.arange(total, device=self.device) - offsets[sid]
+            tok = out.recompute_idx.view(-1).index_select(0, sid * n + pos).long()
+            flat = sid * n + tok
+            x = m.embed(self._embed_input(frames, flat, dt)) + m.pos.index_select(0, tok)   # [T, D] layer 0
         if self.mode == "layer1":
             blk = m.blocks[0]
             d = m.c.width
@@ -283,19 +310,22 @@ class CachedEncoder:
                 # attention over every token of the stream (one dense SDPA);
                 # only the recomputed tokens' rows are kept
                 q, k, v = (blk._heads(t) for t in self.qkv0[o].split(d, dim=-1))
-                att = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).flatten(-2)   # [B, N, D]
-                x = x + blk.proj(att[sid, tok])
+                att = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B * n, d)
+                x = x + blk.proj(att.index_select(0, flat))
                 x1 = x + blk.fc2(F.gelu(blk.fc1(blk.ln2(x)), approximate="tanh"))
             else:
                 x1 = torch.zeros((1, d), dtype=dt, device=self.device)
             splice_packed(out.src_map, self.h1[i], self.ages[i], x1, offsets[:B].contiguous(), self.h1[o],
                           self.ages[o], status=self.status)
+            self._prefetch(next_frames, cfg, refresh_shift)
             if marks is not None:
                 marks[-1][1].record(main)
             y = self._tail(o)
             if marks is not None:
                 marks[-1][2].record(main)
         else:
+            # the whole packed encoder follows: the next select goes beside it
+            self._prefetch(next_frames, cfg, refresh_shift)
             if total == 0:
                 packed = torch.zeros((1, m.c.width), dtype=dt, device=self.device)
             else:
@@ -312,6 +342,77 @@ class CachedEncoder:
             y = self.h1[o]
         self.cur = o
         return y, out
+
+    def _prefetch(self, next_frames, cfg, refresh_shift):
+        """Issue the next step's select once this step's partial (block-0 /
+        packed) work is enqueued: it then runs beside the long static tail
+        instead of competing with the next step's block-0 work."""
+        if next_frames is not None:
+            self.pending = (next_frames, self._issue_select(next_frames, cfg, refresh_shift))
+
+    def _block0_static(self, tp, o):
+        """Packed block-0 work of one step on the static buffers, for tp
+        (>= the step's recomputed rows) packed rows: gathers, embedding, LN,
+        QKV, the q|k|v splice, dense attention, projection + MLP for the
+        recomputed rows, the block-0 output splice.  Rows past the step's
+        count compute throw-away values that no splice reads."""
+        m, B = self.m, self.B
+        n, d = m.c.tokens, m.c.width
+        dt = next(m.parameters()).dtype
+        i = 1 - o
+        blk = m.blocks[0]
+        offsets = self.st_offsets
+        ar = torch.arange(tp, device=self.device)
+        sid = torch.searchsorted(offsets[1:], ar, right=True).clamp_(max=B - 1)
+        pos = (ar - offsets[sid]).clamp_(0, n - 1)
+        tok = self.st_rec.view(-1).index_select(0, sid * n + pos).long().clamp_(min=0)
+        flat = sid * n + tok                                     # token b * N + p of each packed row
+        x = m.embed(self._embed_input(self.st_frames, flat, dt)) + m.pos.index_select(0, tok)
+        qkv = F.linear(blk.ln1(x), blk.qkv.weight, blk.qkv.bias)
+        splice_packed(self.st_src, self.qkv0[i], self.ages[i], qkv, offsets[:B], self.qkv0[o], self.scratch_ages,
+                      status=self.status)
+        q, k, v = (blk._heads(t) for t in self.qkv0[o].split(d, dim=-1))   # reused rows' q: never read back
+        att = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(B * n, d)
+        x = x + blk.proj(att.index_select(0, flat))
+        x1 = x + blk.fc2(F.gelu(blk.fc1(blk.ln2(x)), approximate="tanh"))
+        splice_packed(self.st_src, self.h1[i], self.ages[i], x1, offsets[:B], self.h1[o], self.ages[o],
+                      status=self.status)
+
+    def _embed_input(self, frames, flat, dt):
+        """Patch pixels of the packed tokens: gathered straight from fp32 RGB
+        frames in bf16 (``fc_gather_patches``), else through torch."""
+        c = self.m.c
+        if dt == torch.bfloat16 and frames.dtype == torch.float32 and frames.is_contiguous():
+            return gather_patches(frames, c.patch, flat)
+        return self.m.patches(frames.to(dt)).reshape(-1, 3 * c.patch * c.patch).index_select(0, flat)
+
+    def _block0_graph(self, tp, o):
+        key = (tp, o)
+        g = self.b0_graphs.get(key)
+        if g is None:
+            # warm-up (library plans) outside capture; harmless before the
+            # first step (prepare_graphs), when the caches hold no state yet
+            st = torch.cuda.Stream(self.device)
+            st.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(st):
+                self._block0_static(tp, o)
+            torch.cuda.current_stream(self.device).wait_stream(st)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=self._pool):
+                self._block0_static(tp, o)
+            self.b0_graphs[key] = g
+        return g
+
+    def prepare_graphs(self):
+        """Capture every block-0 bucket graph up front (no capture inside a
+        timed loop)."""
+        if self.b0_graphs is None:
+            return
+        with torch.no_grad():
+            nb = self.B * self.m.c.tokens
+            for tp in range(self.bucket, -(-nb // self.bucket) * self.bucket + 1, self.bucket):
+                for o in (0, 1):
+                    self._block0_graph(tp, o)
 
     def _tail(self, o):
         """Blocks 1.. and the final LN on every token of cache buffer o —

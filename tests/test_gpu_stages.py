@@ -548,3 +548,21 @@ def test_fused_cluster_colsinv_matches_split_kernels(cuda, monkeypatch, streams)
                         rep=rep)
     assert torch.equal(split.state, fused.state)
     assert rep.ok, rep.errors
+
+
+def test_gather_patches_matches_torch_patchify(cuda):
+    """fc_gather_patches (config 4's recomputed-token pixels, straight from
+    fp32 RGB frames to bf16) equals torch's patchify + cast + row gather bit
+    for bit, including ragged, repeated and boundary token indices."""
+    import torch
+    from paper_2604_24391_b200.engine import gather_patches
+    from paper_2604_24391_b200.vit import ViT, ViTConfig
+    c = ViTConfig(image=112, patch=14, width=64, mlp=128, heads=2, layers=1)
+    model = ViT(c).cuda().eval()
+    g = torch.Generator(device="cuda").manual_seed(4)
+    frames = torch.rand((5, 112, 112, 3), generator=g, device="cuda")
+    n = c.tokens
+    idx = torch.tensor([0, n - 1, n, 3 * n + 17, 5 * n - 1, 17, 17, 2 * n + 33], dtype=torch.int64, device="cuda")
+    got = gather_patches(frames, 14, idx)
+    ref = model.patches(frames.to(torch.bfloat16)).reshape(-1, 3 * 14 * 14).index_select(0, idx)
+    assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
