@@ -305,7 +305,7 @@ def test_config2_sweep_16_streams(cuda):
     oc.refresh_shift = 1
     eng = fc.FreqCacheEngine(S, 448, 448, 14, fmt="rgb")
     rep = ParityReport()
-    n_exact = 0
+    n_exact = n_pairs = 0
     for t in range(T):
         out = eng.select(torch.from_numpy(np.ascontiguousarray(frames[t])).cuda(), c, refresh_shift=1)
         if t == 0:
@@ -318,8 +318,14 @@ def test_config2_sweep_16_streams(cuda):
             o = O.decide(frames[t - 1, s], frames[t, s], oc, step=t)
             compare(d, o, oc, energies=en[s], rep=rep)
             n_exact += tuple(d.reuse_set) == o.reuse_set and tuple(d.refresh_set) == o.refresh_set
+            n_pairs += max(0, len(o.reuse_set) - 1)
     assert rep.ok, rep.errors
-    print(f"config-2 sweep: {n_exact}/{S * (T - 1)} decisions identical to the oracle; exemptions {rep.exemptions}")
+    # bounded exemptions: only reuse-order swaps between tie-margin energies,
+    # a small fraction of all neighbouring reused pairs
+    assert set(rep.exemptions) <= {"order"}, rep.exemptions
+    assert rep.exemptions.get("order", 0) <= 0.05 * n_pairs, (rep.exemptions, n_pairs)
+    print(f"config-2 sweep: {n_exact}/{S * (T - 1)} decisions identical to the oracle; exemptions {rep.exemptions} "
+          f"of {n_pairs} neighbouring reused pairs")
 
 
 def test_acceptance_shift_recovery_and_latency(cuda):
