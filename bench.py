@@ -600,6 +600,10 @@ def run_ours(a):
         win_main = clocks.stop()
         gpu_launches = launches[0]
         ms = ev0.elapsed_time(ev1)
+        t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_max, op=dist.ReduceOp.MAX)   # every rank sizes the sustained leg alike
+        ms = float(t_max.item())
         cnt_dev = counters.clone()
         # ---- sustained leg: the same steps for >= --sustained-s seconds, with
         # its own clock record (the short default region runs at burst clocks)
@@ -622,10 +626,6 @@ def run_ours(a):
                          "seconds": sms / 1e3, "ms_per_step": sms / n_s, "clocks": clocks.summary(win_s)}
     finally:
         clocks.__exit__(None, None, None)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms = float(t_max.item())
     frames_total = total_streams * a.steps
     value = frames_total / (ms / 1e3)
 
