@@ -457,7 +457,7 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     pl->slot_T = align_up(pl->lane_t1 * pl->lanes);
     pl->off_T2 = off + 2 * pl->slot_T;
     off = pl->off_T2 + align_up(pl->lane_t2 * pl->lanes);
-    specElems = B * 224 * kStCol * 2;  // register-order state (float2 count)
+    specElems = B * 224 * kStColG * 2;  // register-order state (float2 count)
   } else {
     pl->chunk = g.batch;
     const int maxpairC = (kp.RG + 1) / 2;

@@ -62,11 +62,11 @@ __global__ void __cluster_dims__(kClusterBC, 1, 1) __launch_bounds__(32 * kWarps
 #pragma unroll 1
   for (int it = 0; it < 2; ++it) {
     const int q = 28 * r + wid + 14 * it;
-    float4* stg = reinterpret_cast<float4*>(kp.spec) + ((size_t)b * 224 + q) * kStCol;
+    float4* stg = reinterpret_cast<float4*>(kp.spec) + ((size_t)b * 224 + q) * kStColG;
     if (lane == 0) {
       tma::fence_async_shared();   // the slot / prev blocks were generic-proxy scratch
       tma::load_tile(slot, kp.T + ((size_t)bl * 224 + q) * 448, 448 * 8, &bar[wid][0]);
-      if (valid) tma::load_tile(prev, stg, kStCol * 16, &bar[wid][1]);
+      if (valid) tma::load_tile(prev, stg, kStColG * 16, &bar[wid][1]);
     }
     __syncwarp();
     tma::bar_wait(&bar[wid][0], it & 1);
@@ -83,7 +83,7 @@ __global__ void __cluster_dims__(kClusterBC, 1, 1) __launch_bounds__(32 * kWarps
       if (h == 0 || h1) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          stg[(h * 4 + i) * 32 + lane] =
+          stg[st_idx(h, i, lane)] =
               make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
       }
     }
@@ -109,7 +109,7 @@ __global__ void __cluster_dims__(kClusterBC, 1, 1) __launch_bounds__(32 * kWarps
         if (h == 0 || h1) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            cur[(h * 4 + i) * 32 + lane] =
+            cur[st_idx(h, i, lane)] =
                 make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
         }
       }
@@ -117,7 +117,7 @@ __global__ void __cluster_dims__(kClusterBC, 1, 1) __launch_bounds__(32 * kWarps
       auto fetch = [](const float4* base, int k) -> float2 {
         const int j2 = k / 56, rem = k - 56 * j2;
         const int g = 8 * (rem % 7) + rem / 7;
-        const float4 t = base[((g >> 5) * 4 + (j2 >> 1)) * 32 + (g & 31)];
+        const float4 t = base[st_idx(g >> 5, j2 >> 1, g & 31)];
         return (j2 & 1) ? make_float2(t.z, t.w) : make_float2(t.x, t.y);
       };
 #pragma unroll
@@ -127,7 +127,7 @@ __global__ void __cluster_dims__(kClusterBC, 1, 1) __launch_bounds__(32 * kWarps
           for (int j2 = 0; j2 < 8; ++j2) {
             const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
             const int km = (448 - k) % 448;
-            const float4 t = prev[(h * 4 + (j2 >> 1)) * 32 + lane];
+            const float4 t = prev[st_idx(h, j2 >> 1, lane)];
             const float2 pk = (j2 & 1) ? make_float2(t.z, t.w) : make_float2(t.x, t.y);
             float2 c0, cn, p0, pn;
             unpack_dcny(v[h][j2], fetch(cur, km), c0, cn);
@@ -145,7 +145,7 @@ __global__ void __cluster_dims__(kClusterBC, 1, 1) __launch_bounds__(32 * kWarps
         if (h == 0 || h1) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const float4 t = prev[(h * 4 + i) * 32 + lane];
+            const float4 t = prev[st_idx(h, i, lane)];
             v[h][2 * i] = acc(make_float2(t.x, t.y), v[h][2 * i]);
             v[h][2 * i + 1] = acc(make_float2(t.z, t.w), v[h][2 * i + 1]);
           }

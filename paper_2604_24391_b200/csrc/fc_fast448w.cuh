@@ -16,7 +16,8 @@
 // Per-stream state (the previous frame's half spectrum) is kept in the
 // register order of K_B's forward transform:
 //   spec [q][h][i][lane] float4 = (X[k(j2 = 2i)], X[k(j2 = 2i + 1)]) of group
-//   g = lane + 32 h, k(j2) = (g >> 3) + 7 (g & 7) + 56 j2  (4 KB per column)
+//   g = lane + 32 h, k(j2) = (g >> 3) + 7 (g & 7) + 56 j2, half 1 holding
+//   only its 24 active lanes (st_idx; 3,584 bytes per column)
 // so a warp loads / stores its column with 16-byte coalesced accesses.
 #pragma once
 #include <type_traits>
@@ -27,9 +28,15 @@ constexpr int kWarpsB = 4;                 // columns (warps) per K_B CTA
 constexpr int kNCB448 = 224 / kWarpsB;     // K_B CTAs per stream = stats partials
 constexpr int kWarpsC = 4;                 // row pairs (warps) per K_C CTA
 constexpr int kNRG448 = 224 / kWarpsC;     // K_C CTAs per stream = peak partials
-constexpr int kStCol = 2 * 4 * 32;         // float4 per state column
+constexpr int kStCol = 2 * 4 * 32;         // float4 per state column block in shared memory
+constexpr int kStColG = 4 * 32 + 4 * 24;   // float4 per state column in HBM: half 1 has 24 lanes
 constexpr int kSlotB = 512;                // float2: T1 column (448), then FFT scratch (504)
 constexpr int kSmemB448 = kWarpsB * (kSlotB * 8 + kStCol * 16);
+
+// float4 index of (half h, pair i, lane) in a state column: half 0 holds
+// lanes 0..31, half 1 only the 24 active lanes (groups g < 56), so the
+// column is 3,584 bytes with nothing unused in HBM
+__device__ __forceinline__ int st_idx(int h, int i, int lane) { return h == 0 ? i * 32 + lane : 128 + i * 24 + lane; }
 static_assert(kWarpsB == 4 && 224 * 4 * 16 + 1023 <= kWarpsB * kStCol * 16, "T2 tile (aligned) must fit the prev blocks");
 constexpr int kSmemC448 = kWarpsC * w448::XS * 8;
 
@@ -65,12 +72,12 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
   float2* slot = reinterpret_cast<float2*>(smem + wid * (kSlotB * 8));
   float4* prev = reinterpret_cast<float4*>(smem + kWarpsB * kSlotB * 8 + wid * (kStCol * 16));
   const bool valid = kp.hdr[b].valid != 0;
-  float4* stg = reinterpret_cast<float4*>(kp.spec) + ((size_t)b * 224 + q) * kStCol;
+  float4* stg = reinterpret_cast<float4*>(kp.spec) + ((size_t)b * 224 + q) * kStColG;
   if (lane == 0) {
     tma::bar_init(&bar[wid][0], 1);
     tma::bar_init(&bar[wid][1], 1);
     tma::load_tile(slot, kp.T + ((size_t)bl * 224 + q) * 448, 448 * 8, &bar[wid][0]);
-    if (valid) tma::load_tile(prev, stg, kStCol * 16, &bar[wid][1]);
+    if (valid) tma::load_tile(prev, stg, kStColG * 16, &bar[wid][1]);
   }
   W448Tw<LAZY> tw;
   tw.load(kp.tw448, kp.tw64, lane);
@@ -92,7 +99,7 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
     if (h == 0 || h1) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        stg[(h * 4 + i) * 32 + lane] = make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
+        stg[st_idx(h, i, lane)] = make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
     }
   }
   if (!valid) return;  // cold stream: spectrum established (block-uniform)
@@ -128,14 +135,14 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
       if (h == 0 || h1) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          cur[(h * 4 + i) * 32 + lane] = make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
+          cur[st_idx(h, i, lane)] = make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
       }
     }
     __syncwarp();
     auto fetch = [](const float4* base, int k) -> float2 {
       const int j2 = k / 56, rem = k - 56 * j2;
       const int g = 8 * (rem % 7) + rem / 7;
-      const float4 t = base[((g >> 5) * 4 + (j2 >> 1)) * 32 + (g & 31)];
+      const float4 t = base[st_idx(g >> 5, j2 >> 1, g & 31)];
       return (j2 & 1) ? make_float2(t.z, t.w) : make_float2(t.x, t.y);
     };
 #pragma unroll
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
         for (int j2 = 0; j2 < 8; ++j2) {
           const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
           const int km = (448 - k) % 448;
-          const float4 t = prev[(h * 4 + (j2 >> 1)) * 32 + lane];
+          const float4 t = prev[st_idx(h, j2 >> 1, lane)];
           const float2 pk = (j2 & 1) ? make_float2(t.z, t.w) : make_float2(t.x, t.y);
           float2 c0, cn, p0, pn;
           unpack_dcny(v[h][j2], fetch(cur, km), c0, cn);
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
       if (h == 0 || h1) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float4 t = prev[(h * 4 + i) * 32 + lane];
+          const float4 t = prev[st_idx(h, i, lane)];
           v[h][2 * i] = acc(make_float2(t.x, t.y), v[h][2 * i]);
           v[h][2 * i + 1] = acc(make_float2(t.z, t.w), v[h][2 * i + 1]);
         }

@@ -770,7 +770,6 @@ __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_sel
   uint8_t* fresh = reinterpret_cast<uint8_t*>(rank + N);  // N
   uint8_t* reuse = fresh + N;                             // N
   uint8_t* cand = reuse + N;                              // N
-  __shared__ double red[32 * 2];
   __shared__ int redi[32];
   __shared__ fc_stream_result R;
   __shared__ int sh_flush, sh_dip, sh_djp, sh_kfinal, sh_err;

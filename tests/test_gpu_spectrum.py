@@ -36,21 +36,22 @@ def _hdr_bytes(batch):
 
 def decode_fast448(state, batch, b):
     """[448, 225] complex128 half spectrum of stream b from the fast path's
-    register-order state: spec[q][h][i][lane] float4 = (X[k(2i)], X[k(2i+1)])
-    of group g = lane + 32 h (< 56), k(j2) = (g >> 3) + 7 (g & 7) + 56 j2;
-    column 0 packs the DC (real part along rows) and Nyquist columns."""
+    register-order state: per column q, half 0 = [4 pairs][32 lanes] float4,
+    half 1 = [4 pairs][24 lanes] float4 (fc_fast448w.cuh st_idx), each float4
+    = (X[k(2i)], X[k(2i+1)]) of group g = lane + 32 h, k(j2) = (g >> 3) +
+    7 (g & 7) + 56 j2; column 0 packs the DC (real along rows) and Nyquist
+    columns."""
     raw = state[_hdr_bytes(batch):].view(np.float32)
-    per = 224 * 2 * 4 * 32 * 4
-    s = raw[b * per:(b + 1) * per].reshape(224, 2, 4, 32, 4)
+    per = 224 * (4 * 32 + 4 * 24) * 4
+    col = raw[b * per:(b + 1) * per].reshape(224, 4 * 32 + 4 * 24, 4)
+    halves = (col[:, :128].reshape(224, 4, 32, 4), col[:, 128:].reshape(224, 4, 24, 4))
     Z = np.zeros((224, 448), dtype=np.complex128)      # [q][k]
     for h in range(2):
-        for lane in range(32):
+        for lane in range(32 if h == 0 else 24):
             g = lane + 32 * h
-            if g >= 56:
-                continue
             base = (g >> 3) + 7 * (g & 7)
             for i in range(4):
-                v = s[:, h, i, lane, :].astype(np.float64)
+                v = halves[h][:, i, lane, :].astype(np.float64)
                 Z[:, base + 56 * (2 * i)] = v[:, 0] + 1j * v[:, 1]
                 Z[:, base + 56 * (2 * i + 1)] = v[:, 2] + 1j * v[:, 3]
     return _unpack(Z.T, 448)
