@@ -823,10 +823,13 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
   const size_t bulk_smem = (size_t)NL * SL * row_bytes + (size_t)(batch + 1) * 4;
   const int use_bulk = env_int("FC_SPLICE_BULK", 1, 0, 1);
   if (use_bulk && bulk_smem <= 96 * 1024) {
-    const int per_sm = env_int("FC_SPLICE_BULK_CTAS", 2, 1, 32);
+    const int per_sm = env_int("FC_SPLICE_BULK_CTAS", 1, 1, 32);
+    // FC_SPLICE_BULK_GRID: absolute copier CTA count (overrides per-SM sizing)
+    const int grid_abs = env_int("FC_SPLICE_BULK_GRID", 0, 0, 1 << 16);
+    const int grid = grid_abs > 0 ? grid_abs : sms * per_sm;
     auto fn = pick_bulk(NL, SL);  // the (NL, SL) instance bulk_smem was sized for
     if (bulk_smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem);
-    fn<<<sms * per_sm, 32, bulk_smem, st>>>(
+    fn<<<grid, 32, bulk_smem, st>>>(
         batch, n_tokens, (int)row_bytes, src_map, reinterpret_cast<char*>(cache0), reinterpret_cast<char*>(cache1),
         ages0, ages1, slot_in, slot_out, rows, counts, reinterpret_cast<const char*>(fresh),
         fresh_layout == FC_FRESH_COMPACT, fresh_rows, status);
