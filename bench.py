@@ -651,6 +651,24 @@ def run_ours(a):
         one_step(t, kms)
     kms = [v / kp_steps for v in kms]
     splice_moved = splice_bytes[0] / kp_steps
+    # the same splice alone with the copier twice as wide (2 CTAs per SM, the
+    # standalone-best sizing): the step's copier is sized to co-run with the
+    # select kernels and leaves them HBM, so alone it is slower
+    wide = [0.0] * 6
+    sb0 = splice_bytes[0]
+    old = os.environ.get("FC_SPLICE_BULK_CTAS")
+    os.environ["FC_SPLICE_BULK_CTAS"] = "2"
+    try:
+        for t in range(t0 + kp_steps, t0 + 2 * kp_steps):
+            one_step(t, wide)
+    finally:
+        if old is None:
+            os.environ.pop("FC_SPLICE_BULK_CTAS", None)
+        else:
+            os.environ["FC_SPLICE_BULK_CTAS"] = old
+    wide_ms = wide[5] / kp_steps
+    wide_bytes = (splice_bytes[0] - sb0) / kp_steps
+    t_next = t0 + 2 * kp_steps
     hw = H * H
     spec = 8 * H * ((H // 2 + 7) // 8) * 8   # one packed half-spectrum, fp32 complex
     kbytes = [
@@ -672,7 +690,12 @@ def run_ours(a):
     moved_ach = (b_sel + splice_moved / S) * frames_per_s_gpu / 1e9
     roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "traffic": None, "kernel": names[dom], "peak_kind": peak_kind,
-                "bytes_per_launch": kbytes[dom], "ms_per_launch": kms[dom]}
+                "bytes_per_launch": kbytes[dom], "ms_per_launch": kms[dom],
+                "note": "serialised pass, each kernel configured as in the timed step; the splice copier is "
+                        "sized to co-run with the select kernels (1 CTA/SM), see splice_alone_wide"}
+    splice_wide = {"ms": wide_ms, "bytes": wide_bytes, "gbs": wide_bytes / (wide_ms / 1e3) / 1e9,
+                   "frac": wide_bytes / (wide_ms / 1e3) / 1e9 / hbm,
+                   "config": "FC_SPLICE_BULK_CTAS=2 (2 copier CTAs per SM), same splices, serialised"}
     roofline_step = {"bound": "hbm", "achieved": step_ach, "peak": hbm, "unit": "GB/s", "frac": step_ach / hbm,
                      "bytes_per_frame": b_sel + b_spl, "select_bytes": b_sel, "splice_bytes": b_spl,
                      "splice_moved_bytes_per_frame": splice_moved / S,
@@ -844,6 +867,7 @@ def run_ours(a):
                              f"{R * S * H * H * 12 / 1e9:.1f} GB ring)"},
             "tokens_per_s": value * N,
             "roofline": roofline, "roofline_step": roofline_step, "kernels": kernels,
+            "splice_alone_wide": splice_wide,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "h2d_gbs": e2e_h2d_gbs, "pcie_copy_gbs": pcie_gbs, "link_frac": e2e_h2d_gbs / pcie_gbs,
