@@ -67,7 +67,7 @@ def parse(argv=None):
     ap.add_argument("--no-pipeline", action="store_true",
                     help="whole select per step (no front/back overlap across steps)")
     ap.add_argument("--cpu-streams", type=int, default=64)
-    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--cpu-kind", default="auto", choices=["auto", "reference", "port"],
                     help="CPU baseline: the reference package (baseline/_ref) or the oracle port")
     ap.add_argument("--no-cpu-baseline", action="store_true")
