@@ -216,3 +216,25 @@ def test_psi_status_maps_to_reference_error():
     rec["entropy_norm"] = 1.0000000000000002
     with pytest.raises(ValueError, match=r"normalized entropy must lie in \[0, 1\], got 1.0000000000000002"):
         _raise_status(rec)
+
+
+def test_new_entry_points_refuse_bad_arguments_without_device(lib):
+    """Round-2 entry points validate on the host before any device call."""
+    import ctypes
+    from paper_2604_24391_b200 import _native
+    p = ctypes.c_void_p(4096)   # never dereferenced
+    E = _native.FC_EINVAL
+    assert lib.fc_select_front(None, None, p, p, None, 0, None) == E
+    assert lib.fc_select_back(None, None, p, p, None, 0, None) == E
+    assert lib.fc_dft2(0, 4, p, 0, 0, p, p, None) == E
+    assert lib.fc_dft2(4, 4, None, 0, 0, p, p, None) == E
+    assert lib.fc_dft2_workspace_bytes(0, 3) == -1
+    assert lib.fc_phase_correlation_spectra(4, 0, p, p, p, p, None) == E
+    assert lib.fc_block_dct(1, 65, p, p, None) == E
+    assert lib.fc_block_dct(0, 8, None, None, None) == _native.FC_OK      # nothing to do
+    assert lib.fc_amplitude_phase(-1, p, p, p, None) == E
+    assert lib.fc_gather_patches(-1, 1, 28, 28, 14, p, p, p, None) == E
+    assert lib.fc_gather_patches(4, 1, 30, 28, 14, p, p, p, None) == E     # P does not divide H
+    assert lib.fc_graph_launch(None, None) == E
+    assert lib.fc_graph_capture_end(None, None) == E
+    assert lib.fc_plan_launches(None) == -1
