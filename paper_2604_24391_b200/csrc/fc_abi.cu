@@ -60,6 +60,7 @@ struct fc_plan {
   bool t2_tma = false;                 // K_B stores T2 with a TMA tensor store
   bool t1_tma = false;                 // K_A stores T1 with a TMA tensor store
   bool fused_bc = false;               // K_B + K_C as one cluster kernel (T2 through DSMEM)
+  int kc_ppw = 1;                      // K_C row pairs per warp
   void* fnC = nullptr;
   float2* d_twW = nullptr;
   float2* d_twH = nullptr;
@@ -332,7 +333,7 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
         fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm2[l]);
         if (rec) rec->mark(st, 1);
         auto fc = (void (*)(KParams, int))pl->fnC;
-        fc<<<dim3(kNRG448, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
+        fc<<<dim3(kNRG448 / pl->kc_ppw, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
         if (rec) rec->mark(st, 2);
       }
     }
@@ -443,12 +444,15 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
     if (pl->lanes > nchunks) pl->lanes = nchunks;
     pl->smemA = (size_t)kPxBytes448;
     pl->smemB = (size_t)kSmemB448;
-    pl->smemC = (size_t)kSmemC448;
+    pl->smemC = (size_t)kSmemC448 * env_int("FC_KC_PPW", 1, 1, 2);
     // K_B / K_C, or the fused cluster kernel K_BC (FC_FUSED_BC=1), whose
     // partials are one per column / one per warp
     pl->fused_bc = env_int("FC_FUSED_BC", 0, 0, 1) != 0;
+    // K_C row pairs per warp (FC_KC_PPW): 2 shares twiddles, gather indices
+    // and reductions between two transforms
+    pl->kc_ppw = env_int("FC_KC_PPW", 1, 1, 2);
     kp.NCB = pl->fused_bc ? kNCBf : kNCB448;   // stats partials per stream
-    kp.NRG = pl->fused_bc ? kNRGf : kNRG448;   // peak partials per stream
+    kp.NRG = pl->fused_bc ? kNRGf : kNRG448 / pl->kc_ppw;   // peak partials per stream
     // [T1 slot 0: lanes x chunk streams | T1 slot 1 | T2], lanes contiguous
     // inside each, so a launch over the whole batch can also address them
     pl->lane_t1 = (size_t)pl->chunk * 224 * 448 * sizeof(float2);
@@ -557,8 +561,11 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
                                                                             : (void*)k448_cols<4, false, true>)
                            : (ob >= 6 ? (void*)k448_cols<6, true, false> : ob == 5 ? (void*)k448_cols<5, false, false>
                                                                              : (void*)k448_cols<4, false, false>);
-      pl->fnC = oc >= 10 ? (void*)k448_rows_inv<10, true> : oc >= 8 ? (void*)k448_rows_inv<8, true>
-              : oc == 7 ? (void*)k448_rows_inv<7, true> : (void*)k448_rows_inv<6, false>;
+      if (pl->kc_ppw == 2)
+        pl->fnC = oc >= 7 ? (void*)k448_rows_inv<7, true, 2> : (void*)k448_rows_inv<6, true, 2>;
+      else
+        pl->fnC = oc >= 10 ? (void*)k448_rows_inv<10, true> : oc >= 8 ? (void*)k448_rows_inv<8, true>
+                : oc == 7 ? (void*)k448_rows_inv<7, true> : (void*)k448_rows_inv<6, false>;
       if (rc == FC_OK) rc = set_smem(pl->fnB, pl->smemB);
       if (rc == FC_OK) rc = set_smem(pl->fnC, pl->smemC);
       if (rc == FC_OK && pl->fused_bc) rc = set_smem((void*)k448_colsinv<true>, kSmemBC);

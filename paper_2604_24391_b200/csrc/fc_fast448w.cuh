@@ -229,12 +229,14 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
 }
 
 // ------------------------------------------------------------- K_C 448 ----
-// One warp per row pair (ya, ya + 1) of T2: both rows are one packed complex
-// 448-point inverse transform (c2r), read straight from the L2-resident T2
-// row-pair block (one 16-byte load gives both rows of a column).  Then the
-// argmax with the reference's tie rule and the runner-up; one peak partial
-// per CTA (kNRG448 per stream), merged by K_D in its fixed tie order.
-template <int MINB, bool LAZY>
+// One warp per PPW row pairs (ya, ya + 1) of T2: both rows of a pair are one
+// packed complex 448-point inverse transform (c2r), read from the pair's
+// contiguous T2 block (one 16-byte load gives both rows of a column).  Then
+// the argmax with the reference's tie rule and the runner-up; one peak partial
+// per CTA (224 / (kWarpsC PPW) per stream), merged by K_D in its fixed tie
+// order.  With PPW = 2 a warp's two blocks arrive in one bulk-copy phase and
+// its twiddles, gather indices and reductions serve both pairs.
+template <int MINB, bool LAZY, int PPW = 1>
 __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, int b0) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ PeakKey redk[kWarpsC];
@@ -243,84 +245,93 @@ __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, 
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bl = blockIdx.y, b = b0 + bl;
   if (kp.hdr[b].valid == 0) return;  // cold stream (block-uniform)
-  const int pair = blockIdx.x * kWarpsC + wid;
-  const int ya = 2 * pair;
-  float2* S = reinterpret_cast<float2*>(smem) + wid * w448::XS;
-  const float4* T2 = reinterpret_cast<const float4*>(kp.T2) + ((size_t)bl * 224 + pair) * 224;
-  // the row pair's 3.5 KB T2 block lands in the warp's FFT scratch with one
-  // bulk copy; the lanes then gather their (mirrored) columns from shared memory
+  const int pair0 = (blockIdx.x * kWarpsC + wid) * PPW;
+  float2* S0 = reinterpret_cast<float2*>(smem) + wid * PPW * w448::XS;
+  const float4* T2 = reinterpret_cast<const float4*>(kp.T2) + ((size_t)bl * 224 + pair0) * 224;
+  // each row pair's 3.5 KB T2 block lands in its own FFT scratch region with
+  // one bulk copy; the lanes then gather their (mirrored) columns from there
   if (lane == 0) {
     tma::bar_init(&barc[wid], 1);
-    tma::load_tile(S, T2, 224 * 16, &barc[wid]);
-  }
-  __syncwarp();
-  tma::bar_wait(&barc[wid], 0);
-  const float4* Sb = reinterpret_cast<const float4*>(S);
-  const int k1a = lane >> 3, j1 = lane & 7;
-  float4 in[2][8];
+    tma::bar_expect(&barc[wid], PPW * 224 * 16);
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (h == 0 || lane < 24) {
-#pragma unroll
-      for (int j2 = 0; j2 < 8; ++j2) {
-        const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
-        const int qq = (k == 0 || k == 224) ? 0 : (k < 224 ? k : 448 - k);
-        in[h][j2] = Sb[qq];
-      }
-    }
+    for (int i = 0; i < PPW; ++i) tma::bulk_g2s(S0 + i * w448::XS, T2 + i * 224, 224 * 16, &barc[wid]);
   }
-  __syncwarp();  // block consumed: S becomes FFT scratch
   W448Tw<LAZY> tw;
   tw.load(kp.tw448, kp.tw64, lane);
-  float2 v[2][8], a[2][7];
+  __syncwarp();
+  tma::bar_wait(&barc[wid], 0);
+  const int k1a = lane >> 3, j1 = lane & 7;
+  PeakKey best = {-CUDART_INF_F, 0x7fffffff, 0x7fffffff};
+  float v2 = -CUDART_INF_F;
+#pragma unroll 1
+  for (int it = 0; it < PPW; ++it) {
+    const int ya = 2 * (pair0 + it);
+    float2* S = S0 + it * w448::XS;
+    const float4* Sb = reinterpret_cast<const float4*>(S);
+    float4 in[2][8];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (h == 0 || lane < 24) {
+    for (int h = 0; h < 2; ++h) {
+      if (h == 0 || lane < 24) {
 #pragma unroll
-      for (int j2 = 0; j2 < 8; ++j2) {
-        const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
-        const float4 t = in[h][j2];  // (A = row ya, B = row ya + 1) at the column
-        float2 z;
-        if (k == 0) z = make_float2(t.x, t.z);
-        else if (k == 224) z = make_float2(t.y, t.w);
-        else if (k < 224) z = make_float2(t.x - t.w, t.y + t.z);   // G_a + i G_b
-        else z = make_float2(t.x + t.w, t.z - t.y);                // conj G_a + i conj G_b
-        v[h][j2] = z;
+        for (int j2 = 0; j2 < 8; ++j2) {
+          const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
+          const int qq = (k == 0 || k == 224) ? 0 : (k < 224 ? k : 448 - k);
+          in[h][j2] = Sb[qq];
+        }
       }
     }
-  }
-  w448::inv<true>(v, a, S, lane, tw);
-
-  // argmax with the reference tie rule (migration.py:141-159)
-  float m1 = -CUDART_INF_F, m2 = -CUDART_INF_F;
-  int ai = 0;
+    __syncwarp();  // block consumed: S becomes FFT scratch
+    float2 v[2][8], a[2][7];
 #pragma unroll
-  for (int qv = 0; qv < 28; ++qv) {
-    const float2 c = a[qv / 14][(qv % 14) >> 1];
-    const float val = (qv & 1) ? c.y : c.x;
-    if (val > m1) { m2 = m1; m1 = val; ai = qv; }
-    else m2 = fmaxf(m2, val);
-  }
-  auto key_of = [&](int qv, float val) {
-    PeakKey c;
-    const int y = ya + (qv & 1), j = 64 * ((qv % 14) >> 1) + lane + 32 * (qv / 14);
-    c.v = val;
-    c.l1 = abs(canon_disp(y, 448)) + abs(canon_disp(j, 448));
-    c.pos = y * 448 + j;
-    return c;
-  };
-  PeakKey best = key_of(ai, m1);
-  if (m2 == m1) {
+    for (int h = 0; h < 2; ++h) {
+      if (h == 0 || lane < 24) {
+#pragma unroll
+        for (int j2 = 0; j2 < 8; ++j2) {
+          const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
+          const float4 t = in[h][j2];  // (A = row ya, B = row ya + 1) at the column
+          float2 z;
+          if (k == 0) z = make_float2(t.x, t.z);
+          else if (k == 224) z = make_float2(t.y, t.w);
+          else if (k < 224) z = make_float2(t.x - t.w, t.y + t.z);   // G_a + i G_b
+          else z = make_float2(t.x + t.w, t.z - t.y);                // conj G_a + i conj G_b
+          v[h][j2] = z;
+        }
+      }
+    }
+    w448::inv<true>(v, a, S, lane, tw);
+
+    // argmax with the reference tie rule (migration.py:141-159)
+    float m1 = -CUDART_INF_F, m2 = -CUDART_INF_F;
+    int ai = 0;
+#pragma unroll
     for (int qv = 0; qv < 28; ++qv) {
       const float2 c = a[qv / 14][(qv % 14) >> 1];
       const float val = (qv & 1) ? c.y : c.x;
-      if (val == m1) {
-        const PeakKey kq = key_of(qv, val);
-        if (peak_better(kq, best)) best = kq;
+      if (val > m1) { m2 = m1; m1 = val; ai = qv; }
+      else m2 = fmaxf(m2, val);
+    }
+    auto key_of = [&](int qv, float val) {
+      PeakKey c;
+      const int y = ya + (qv & 1), j = 64 * ((qv % 14) >> 1) + lane + 32 * (qv / 14);
+      c.v = val;
+      c.l1 = abs(canon_disp(y, 448)) + abs(canon_disp(j, 448));
+      c.pos = y * 448 + j;
+      return c;
+    };
+    PeakKey cand = key_of(ai, m1);
+    if (m2 == m1) {
+      for (int qv = 0; qv < 28; ++qv) {
+        const float2 c = a[qv / 14][(qv % 14) >> 1];
+        const float val = (qv & 1) ? c.y : c.x;
+        if (val == m1) {
+          const PeakKey kq = key_of(qv, val);
+          if (peak_better(kq, cand)) cand = kq;
+        }
       }
     }
+    if (peak_better(cand, best)) { v2 = fmaxf(fmaxf(v2, m2), best.v); best = cand; }
+    else v2 = fmaxf(fmaxf(v2, m2), cand.v);
   }
-  float v2 = m2;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     PeakKey other;
@@ -343,6 +354,6 @@ __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, 
     }
     PeakPart pp;
     pp.v = best.v; pp.v2 = v2; pp.y = best.pos / 448; pp.j = best.pos % 448;
-    kp.peaks[(size_t)b * kNRG448 + blockIdx.x] = pp;
+    kp.peaks[(size_t)b * (kNRG448 / PPW) + blockIdx.x] = pp;
   }
 }
