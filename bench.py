@@ -266,8 +266,13 @@ def run_plumbing(a):
         dist.all_gather(spans, torch.tensor([lo, hi], dtype=torch.int64))
     else:
         spans = [torch.tensor([lo, hi])]
+    # the weak leg beside a strong headline: --streams per rank
+    wlo, whi = (rank * a.streams, (rank + 1) * a.streams) if not a.weak else (lo, hi)
+    wms = max_over_ranks(2.0 + rank)
     if rank == 0:
         print(json.dumps({"metric": METRIC, "plumbing": True, "n_gpus": world, "ms_max": ms,
+                          "weak_scaling": {"ms_max": wms, "span0": [wlo, whi],
+                                           "streams_total": a.streams * world},
                           "streams_total": total, "streams_per_rank": [int(s[1] - s[0]) for s in spans],
                           "spans": [[int(s[0]), int(s[1])] for s in spans], "frames": cnt["frames"],
                           "scaling": "weak" if a.weak else "strong"}), flush=True)
@@ -362,6 +367,159 @@ def peaks():
         return 6650.0, "fallback"
 
 
+class Pipeline:
+    """One rank's pipelined config-5 step on the GPU: resident frame ring,
+    token caches, the engine and the in-place splice state, and the step
+    replayed from CUDA graphs.  Step t = the front of select t + 1 (K_A,
+    K_D1; workspace slot (t + 1) & 1) beside the back of select t (K_B, K_C,
+    K_D; slot t & 1) beside the in-place splice of step t - 1, each on its
+    own stream, joined at the end of the step.  Select outputs are
+    double-buffered: the front of t + 1 writes only the energies of buffer
+    (t + 1) & 1 while the splice of t - 1 reads that buffer's splice map.
+    --no-pipeline: select(t) as one call beside the splice of t - 1.
+    --graph-steps G > 1: chunks of G steps per graph without per-step joins
+    (every branch waits only on the events of the work it depends on)."""
+
+    def __init__(self, a, dev, S, lo, rank, R):
+        import torch
+
+        from paper_2604_24391_b200 import CacheConfig, FreqCacheEngine, SpliceState, StepGraph
+        from paper_2604_24391_b200.synth import torch_stream_frames
+        H, P, D = a.size, a.patch, a.dim
+        N = (H // P) ** 2
+        self.a, self.dev, self.R = a, dev, R
+        self.cfg = cfg = CacheConfig(patch_size=P)
+        # inputs, resident in HBM before timing (untimed generation); this
+        # rank's streams are its contiguous block [lo, lo + S) of the job's
+        self.frames = frames = torch.empty((R, S, H, H, 3), dtype=torch.float32, device=dev)
+        for c0 in range(0, S, 64):
+            c1 = min(S, c0 + 64)
+            frames[:, c0:c1] = torch_stream_frames(c1 - c0, R, H, H, seed=5000 + lo + c0, device=dev)
+        g = torch.Generator(device=dev).manual_seed(3000 + rank)
+        cache = torch.empty((2, S, N, D), dtype=torch.bfloat16, device=dev)
+        cache[0].normal_(generator=g)
+        self.fresh = fresh = torch.empty((S, N, D), dtype=torch.bfloat16, device=dev).normal_(generator=g)
+        ages = torch.zeros((2, S, N), dtype=torch.int64, device=dev)
+        self.eng = eng = FreqCacheEngine(S, H, H, P, fmt="rgb", device=dev)
+        self.spl = spl = SpliceState(cache, ages)   # in place where the displacement is zero, else ping-pong
+        # run_sequence aggregates over the timed steps, accumulated by the
+        # select kernel itself (frames, reused tokens, flushes, cold)
+        self.counters = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.outs = outs = [eng.out, eng.new_output()]
+        for o in outs:
+            o.counters = self.counters
+        torch.cuda.synchronize()
+        self.launches = [0]
+        self.per_phase = (eng.launches_per_select if a.no_pipeline else eng.launches_per_split_step) + 2
+        self.n_spliced = n_spliced = [0]   # splices issued so far: SpliceState's ping-pong parity
+        side = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_SIDE_PRIO", "-1")))
+        fs = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_FRONT_PRIO", "0")))
+        bs = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_BACK_PRIO", "0")))
+        rs = a.refresh_shift
+
+        def phase(t):
+            cur = torch.cuda.current_stream(dev)
+            side.wait_stream(cur)
+            if a.no_pipeline:
+                eng.select(frames[t % R], cfg, out=outs[t & 1], refresh_shift=rs)
+            else:
+                if t == 0:
+                    eng.select_front(frames[0], cfg, outs[0], 0, refresh_shift=rs)
+                fs.wait_stream(cur)
+                with torch.cuda.stream(fs):
+                    eng.select_front(frames[(t + 1) % R], cfg, outs[(t + 1) & 1], (t + 1) & 1, refresh_shift=rs)
+                bs.wait_stream(cur)
+                with torch.cuda.stream(bs):
+                    eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=rs)
+                cur.wait_stream(bs)
+            if t > 0:
+                with torch.cuda.stream(side):
+                    spl.step(outs[(t - 1) & 1].src_map, fresh)
+                n_spliced[0] += 1
+                cur.wait_stream(side)
+            if not a.no_pipeline:
+                cur.wait_stream(fs)
+
+        ev = {k: [torch.cuda.Event(), torch.cuda.Event()] for k in ("front", "back", "splice")}
+        live = set()   # (kind, parity) recorded inside the current capture
+
+        def wait(stream, kind, t):
+            if t >= 0 and (kind, t & 1) in live:
+                stream.wait_event(ev[kind][t & 1])
+
+        def mark(stream, kind, t):
+            ev[kind][t & 1].record(stream)
+            live.add((kind, t & 1))
+
+        def chunk(t0, n):
+            cur = torch.cuda.current_stream(dev)
+            live.clear()
+            for st_ in (fs, bs, side):
+                st_.wait_stream(cur)
+            for t in range(t0, t0 + n):
+                wait(fs, "back", t - 1)
+                with torch.cuda.stream(fs):
+                    eng.select_front(frames[(t + 1) % R], cfg, outs[(t + 1) & 1], (t + 1) & 1, refresh_shift=rs)
+                mark(fs, "front", t + 1)
+                wait(side, "back", t - 1)
+                with torch.cuda.stream(side):
+                    spl.step(outs[(t - 1) & 1].src_map, fresh)
+                n_spliced[0] += 1
+                mark(side, "splice", t - 1)
+                wait(bs, "front", t)
+                wait(bs, "splice", t - 2)
+                with torch.cuda.stream(bs):
+                    eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=rs)
+                mark(bs, "back", t)
+            for st_ in (fs, bs, side):
+                cur.wait_stream(st_)
+
+        self.phase = phase
+        # CUDA graphs: one per ring phase (frames[t % R], outs[t & 1] and the
+        # splice ping-pong parity repeat with period R), and one per chunk of
+        # G phases starting at t = 1 (mod G), G dividing R
+        self.graphs = self.chunk_graphs = None
+        self.G = G = a.graph_steps if (a.graph_steps > 1 and R % a.graph_steps == 0 and not a.no_pipeline) else 1
+        phase(0)                                   # step 0 establishes every stream's spectrum
+        self.t_next = 1
+        if not a.no_graph:
+            base = n_spliced[0]
+            self.graphs = []
+            for p in range(R):
+                t = self.t_next + p
+                spl.k = (base + (t - 1)) & 1      # the parity splice(t - 1) has at replay
+                self.graphs.append(StepGraph(lambda t=t: phase(t), device=dev))
+            if G > 1:
+                self.chunk_graphs = []
+                for c0 in range(1, R + 1, G):
+                    spl.k = (base + (c0 - 1)) & 1
+                    self.chunk_graphs.append(StepGraph(lambda c0=c0: chunk(c0, G), device=dev))
+            n_spliced[0] = base
+            spl.k = base & 1
+            torch.cuda.synchronize()
+
+    def advance(self, n):
+        """n pipelined steps from t_next (whole chunks where aligned)."""
+        R, G = self.R, self.G
+        while n > 0:
+            t = self.t_next
+            if self.chunk_graphs is not None and (t - 1) % G == 0 and n >= G:
+                self.chunk_graphs[((t - 1) % R) // G].replay()
+                k = G
+            elif self.graphs is not None:
+                self.graphs[(t - 1) % R].replay()
+                k = 1
+            else:
+                self.phase(t)
+                k = 1
+            if self.graphs is not None:
+                self.n_spliced[0] += k
+                self.spl.k = self.n_spliced[0] & 1
+            self.launches[0] += self.per_phase * k
+            self.t_next += k
+            n -= k
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -382,86 +540,19 @@ def run_ours(a):
         else:
             dist.init_process_group(backend)
 
-    from paper_2604_24391_b200 import CacheConfig, FreqCacheEngine, SpliceState, StepGraph
-    from paper_2604_24391_b200.synth import torch_stream_frames
+    from paper_2604_24391_b200 import CacheConfig, FreqCacheEngine, SpliceState
 
     H, P, D, R = a.size, a.patch, a.dim, a.ring + (a.ring & 1)
     total_streams = a.streams * world if a.weak else a.streams
     N = (H // P) ** 2
     cfg = CacheConfig(patch_size=P)
 
-    # ---- inputs, resident in HBM before timing (untimed generation); this
-    # rank's streams are its contiguous block of the job's streams
     from paper_2604_24391_b200.dist import gather_counters, shard
     lo, hi = shard(total_streams, world, rank)
     S = hi - lo
-    frames = torch.empty((R, S, H, H, 3), dtype=torch.float32, device=dev)
-    chunk = 64
-    for c0 in range(0, S, chunk):
-        c1 = min(S, c0 + chunk)
-        frames[:, c0:c1] = torch_stream_frames(c1 - c0, R, H, H, seed=5000 + lo + c0, device=dev)
-    g = torch.Generator(device=dev).manual_seed(3000 + rank)
-    cache = torch.empty((2, S, N, D), dtype=torch.bfloat16, device=dev)
-    cache[0].normal_(generator=g)
-    splice_bytes = [0]
-    fresh = torch.empty((S, N, D), dtype=torch.bfloat16, device=dev).normal_(generator=g)
-    ages = torch.zeros((2, S, N), dtype=torch.int64, device=dev)
-    eng = FreqCacheEngine(S, H, H, P, fmt="rgb", device=dev)
-    spl = SpliceState(cache, ages)   # in place where the displacement is zero, else ping-pong
-    # run_sequence aggregates over the timed steps, accumulated by the select
-    # kernel itself (frames, reused tokens, flushes, cold)
-    counters = torch.zeros(4, dtype=torch.int64, device=dev)
-    outs = [eng.out, eng.new_output()]
-    for o in outs:
-        o.counters = counters
-    torch.cuda.synchronize()
-
-    launches = [0]
-    per_phase = (eng.launches_per_select if a.no_pipeline else eng.launches_per_split_step) + 2  # + splice plan, copier
-    main = torch.cuda.current_stream(dev)
-    side = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_SIDE_PRIO", "-1")))  # splice CTAs jump the select queue
-    n_spliced = [0]   # splices issued so far: SpliceState's ping-pong parity
-
-    # front-of-next-step and back-of-this-step branches (priorities: knobs)
-    fs = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_FRONT_PRIO", "0")))
-    bprio = os.environ.get("FC_BENCH_BACK_PRIO")
-    bs = torch.cuda.Stream(dev, priority=int(bprio)) if bprio is not None else None
-
-    def phase(t):
-        """Pipelined step t on the current stream, three branches joined at
-        the end: the back half of select(t) (column FFTs, phase correlation,
-        decision; workspace slot t & 1), the front half of select(t + 1)
-        (energies, refresh mask, token order, row FFTs of the next frames;
-        slot (t + 1) & 1) and the splice of step t - 1 (high-priority side
-        stream).  Select outputs are double-buffered: the front of t + 1
-        writes only the energies of buffer (t + 1) & 1 while the splice of
-        t - 1 reads that buffer's splice map.  --no-pipeline: select(t) as
-        one call beside the splice of t - 1."""
-        cur = torch.cuda.current_stream(dev)
-        side.wait_stream(cur)
-        if a.no_pipeline:
-            eng.select(frames[t % R], cfg, out=outs[t & 1], refresh_shift=a.refresh_shift)
-        else:
-            if t == 0:
-                eng.select_front(frames[0], cfg, outs[0], 0, refresh_shift=a.refresh_shift)
-            fs.wait_stream(cur)
-            with torch.cuda.stream(fs):
-                eng.select_front(frames[(t + 1) % R], cfg, outs[(t + 1) & 1], (t + 1) & 1,
-                                 refresh_shift=a.refresh_shift)
-            if bs is None:
-                eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=a.refresh_shift)
-            else:
-                bs.wait_stream(cur)
-                with torch.cuda.stream(bs):
-                    eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=a.refresh_shift)
-                cur.wait_stream(bs)
-        if t > 0:
-            with torch.cuda.stream(side):
-                spl.step(outs[(t - 1) & 1].src_map, fresh)
-            n_spliced[0] += 1
-            cur.wait_stream(side)
-        if not a.no_pipeline:
-            cur.wait_stream(fs)
+    pl = Pipeline(a, dev, S, lo, rank, R)
+    frames, eng, spl, outs, fresh, counters = pl.frames, pl.eng, pl.spl, pl.outs, pl.fresh, pl.counters
+    n_spliced, launches, splice_bytes = pl.n_spliced, pl.launches, [0]
 
     def one_step(t, kernel_ms):
         """Serial select + splice with per-kernel timing (events between launches)."""
@@ -490,91 +581,8 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # Chunks of G pipelined steps without per-step joins: the front, back and
-    # splice branches run on their own streams and wait only on the events
-    # of the work they depend on — back(t) on front(t) and on splice(t - 2)
-    # (its output buffer), front(t + 1) on back(t - 1) (its workspace slot),
-    # splice(t - 1) on back(t - 1) — so a branch's tail overlaps the next
-    # step's other branches; the chunk joins once at its end.
-    bs = torch.cuda.Stream(dev)
-    ev = {k: [torch.cuda.Event(), torch.cuda.Event()] for k in ("front", "back", "splice")}
-    live = set()   # (kind, parity) recorded inside the current capture
-
-    def wait(stream, kind, t):
-        if t >= 0 and (kind, t & 1) in live:
-            stream.wait_event(ev[kind][t & 1])
-
-    def mark(stream, kind, t):
-        ev[kind][t & 1].record(stream)
-        live.add((kind, t & 1))
-
-    def chunk(t0, n):
-        cur = torch.cuda.current_stream(dev)
-        live.clear()
-        for st_ in (fs, bs, side):
-            st_.wait_stream(cur)
-        for t in range(t0, t0 + n):
-            wait(fs, "back", t - 1)
-            with torch.cuda.stream(fs):
-                eng.select_front(frames[(t + 1) % R], cfg, outs[(t + 1) & 1], (t + 1) & 1,
-                                 refresh_shift=a.refresh_shift)
-            mark(fs, "front", t + 1)
-            wait(side, "back", t - 1)
-            with torch.cuda.stream(side):
-                spl.step(outs[(t - 1) & 1].src_map, fresh)
-            n_spliced[0] += 1
-            mark(side, "splice", t - 1)
-            wait(bs, "front", t)
-            wait(bs, "splice", t - 2)
-            with torch.cuda.stream(bs):
-                eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=a.refresh_shift)
-            mark(bs, "back", t)
-        for st_ in (fs, bs, side):
-            cur.wait_stream(st_)
-
-    # ---- CUDA graphs: one per ring phase (frames[t % R], outs[t & 1] and
-    # the splice ping-pong parity repeat with period R), and one per chunk
-    # of G phases starting at t = 1 (mod G), G dividing R
-    graphs = chunk_graphs = None
-    G = a.graph_steps if (a.graph_steps > 1 and R % a.graph_steps == 0 and not a.no_pipeline) else 1
-    phase(0)                                   # step 0 establishes every stream's spectrum
-    t_next = 1
-    if not a.no_graph:
-        base = n_spliced[0]
-        graphs = []
-        for p in range(R):
-            t = t_next + p
-            spl.k = (base + (t - 1)) & 1      # the parity splice(t - 1) has at replay
-            graphs.append(StepGraph(lambda t=t: phase(t), device=dev))
-        if G > 1:
-            chunk_graphs = []
-            for c0 in range(1, R + 1, G):
-                spl.k = (base + (c0 - 1)) & 1
-                chunk_graphs.append(StepGraph(lambda c0=c0: chunk(c0, G), device=dev))
-        n_spliced[0] = base
-        spl.k = base & 1
-        torch.cuda.synchronize()
-
     def advance(n):
-        """n pipelined steps from t_next (whole chunks where aligned)."""
-        nonlocal t_next
-        while n > 0:
-            t = t_next
-            if chunk_graphs is not None and (t - 1) % G == 0 and n >= G:
-                chunk_graphs[((t - 1) % R) // G].replay()
-                k = G
-            elif graphs is not None:
-                graphs[(t - 1) % R].replay()
-                k = 1
-            else:
-                phase(t)
-                k = 1
-            if graphs is not None:
-                n_spliced[0] += k
-                spl.k = n_spliced[0] & 1
-            launches[0] += per_phase * k
-            t_next += k
-            n -= k
+        pl.advance(n)
 
     # clock sampling starts before the warm-up, so the GPU does not idle while
     # nvidia-smi starts; only samples inside the timed region are kept
@@ -638,6 +646,7 @@ def run_ours(a):
     flush_rate = cnt["flushes"] / max(cnt["frames"], 1)
 
     # complete the last pipelined step's splice, then the serial pass
+    t_next = pl.t_next
     spl.step(outs[(t_next - 1) & 1].src_map, fresh)
     n_spliced[0] += 1
     torch.cuda.synchronize()
@@ -842,6 +851,34 @@ def run_ours(a):
                              "tokens": n1, "path": "CUDA graph: fc_select + fc_splice_inplace"}
         latency["reference_paper_a100_ms"] = 2.54
 
+    # ---- weak-scaling leg beside the strong headline (N > 1): --streams per
+    # rank (rank r owns streams [r S', (r + 1) S')), its own pipeline, warm-up
+    # and K timed steps, max over ranks.  At N = 1 (or under --weak) it is the
+    # headline's own workload and is not re-run.
+    if world > 1 and not a.weak:
+        sw = a.streams
+        plw = Pipeline(a, dev, sw, rank * sw, rank, R)
+        plw.advance(max(0, a.warmup - 1))
+        barrier()
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        plw.advance(a.steps)
+        w1.record(stream)
+        barrier()
+        wms = torch.tensor([w0.elapsed_time(w1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(wms, op=dist.ReduceOp.MAX)
+        wms = float(wms.item())
+        weak_leg = {"value": sw * world * a.steps / (wms / 1e3), "unit": UNIT, "streams_per_gpu": sw,
+                    "streams_total": sw * world, "steps": a.steps, "ms_per_step": wms / a.steps,
+                    "scaling": "weak", "note": "same pipelined step, --streams per rank; the headline "
+                                               "value is the strong (512 in total) run"}
+        del plw
+        torch.cuda.synchronize()
+    else:
+        weak_leg = {"value": value, "unit": UNIT, "streams_per_gpu": S, "streams_total": total_streams,
+                    "steps": a.steps, "ms_per_step": ms / a.steps, "scaling": "weak",
+                    "note": "N = 1" if world == 1 else "the headline run is itself the weak run (--weak)"}
+
     # ---- CPU baseline (rank 0, N == 1 only)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -860,7 +897,7 @@ def run_ours(a):
             "config": {"workload": (f"config5 {'weak: ' + str(a.streams) + ' streams per GPU' if a.weak else 'as written: ' + str(total_streams) + ' streams in total, ' + str(S) + ' per GPU'}"
                                     ": select + splice, adaptive budget, refresh on shift>1"),
                        "graph": not a.no_graph, "pipeline": not a.no_pipeline,
-                       "graph_steps": G if not a.no_graph else 0,
+                       "graph_steps": pl.G if not a.no_graph else 0,
                        "streams_per_gpu": S, "streams_total": total_streams, "size": H, "channels": 3, "patch": P, "tokens": N,
                        "hidden": D, "hidden_dtype": "bf16", "frame_ring_steps": R,
                        "l2": f"inputs > L2 ({S * H * H * 12 / 1e9:.2f} GB of frames per step, "
@@ -884,6 +921,7 @@ def run_ours(a):
                           "frames": int(cnt["frames"]), "cold": int(cnt["cold"]),
                           "over": "every timed step of every rank (select-kernel counters)"},
             "sustained": sustained,
+            "weak_scaling": weak_leg,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -67,6 +67,10 @@ def test_gpus_flag_launches_ranks(gpus, weak):
     assert [s[0] for s in d["spans"]] == [r * total // gpus for r in range(gpus)]
     assert d["frames"] == total * 3
     assert d["scaling"] == ("weak" if weak else "strong")
+    # the weak-scaling leg reported beside the headline: --streams per rank
+    assert d["weak_scaling"]["ms_max"] == float(gpus + 1)
+    assert d["weak_scaling"]["streams_total"] == 512 * gpus
+    assert d["weak_scaling"]["span0"] == [0, 512]
 
 
 @pytest.mark.gpu
@@ -100,3 +104,27 @@ def test_gpu_arm_json_line():
     dc = d["decisions"]
     assert dc["frames"] == 16 * 4 and 0.0 <= dc["reuse_ratio"] <= 1.0 and 0.0 <= dc["flush_rate"] <= 1.0
     assert d["config"]["graph"] is True
+    assert d["weak_scaling"]["value"] == d["value"] and d["weak_scaling"]["streams_per_gpu"] == 16
+
+
+@pytest.mark.gpu
+def test_gpu_two_ranks_one_device():
+    """The real multi-rank kernel path (not its plumbing stub): 2 ranks over
+    gloo sharing cuda:0 (FC_BENCH_DEVICE), strong headline over 16 streams
+    in total plus the weak leg at 16 per rank.  Not a scaling measurement."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(FC_BENCH_DEVICE="0", FC_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--streams", "16", "--steps", "4", "--warmup", "3", "--ring", "4",
+                        "--e2e-steps", "2", "--sustained-s", "0"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["streams_per_gpu"] == 8
+    assert d["decisions"]["frames"] == 16 * 4                 # counters all-reduced over both ranks
+    w = d["weak_scaling"]
+    assert w["streams_total"] == 32 and w["streams_per_gpu"] == 16 and w["value"] > 0
+    assert abs(w["value"] - 32 / (w["ms_per_step"] / 1e3)) / w["value"] < 1e-6
