@@ -60,6 +60,10 @@ struct fc_plan {
   bool t2_tma = false;                 // K_B stores T2 with a TMA tensor store
   bool t1_tma = false;                 // K_A stores T1 with a TMA tensor store
   bool fused_bc = false;               // K_B + K_C as one cluster kernel (T2 through DSMEM)
+  bool flow_bc = false;                // K_B + K_C as one ticket-ordered flow kernel (T2 through L2)
+  int flow_lag = 8;                    // flow: streams K_C trails K_B by
+  void* fnF = nullptr;
+  size_t off_flow = 0;
   int kc_ppw = 1;                      // K_C row pairs per warp
   void* fnC = nullptr;
   float2* d_twW = nullptr;
@@ -164,6 +168,7 @@ KParams bind(const fc_plan* pl, void* state, void* ws, double* energy, int slot 
   kp.order = reinterpret_cast<int16_t*>(w + pl->off_order + slot * pl->slot_order);
   kp.freshm = w + pl->off_freshm + slot * pl->slot_freshm;
   kp.estats = reinterpret_cast<double*>(w + pl->off_estats + slot * pl->slot_estats);
+  kp.flow = reinterpret_cast<int*>(w + pl->off_flow);
   if (state) {
     uint8_t* s = reinterpret_cast<uint8_t*>(state);
     kp.hdr = reinterpret_cast<StreamHdr*>(s);
@@ -265,7 +270,7 @@ bool split_ok(const fc_plan* pl) {
 
 // Which kernels a call launches: the whole select, or one half of the
 // split-phase select (front: K_A + K_D1 of a step; back: K_B + K_C + K_D).
-enum Part { kAll = 0, kFront = 1, kBack = 2 };
+enum Part { kAll = 0, kFront = 1, kBack = 2, kCols = 3, kTail = 4 };
 
 // Internal lane streams and fork / join events of one part: the front of
 // step t + 1 and the back of step t run concurrently, so they never share a
@@ -281,7 +286,10 @@ struct LaneSet {
 int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, const KParams& kp,
                   const fc_select_out& out, cudaStream_t st, Recorder* rec, Part part = kAll) {
   const int B = pl->g.batch;
-  const bool front = part != kBack, back = part != kFront;
+  const bool front = part == kAll || part == kFront;
+  const bool back = part != kFront;
+  const bool do_b = part == kAll || part == kBack || part == kCols;
+  const bool do_c = part == kAll || part == kBack || part == kTail;
   if (pl->fast) {
     const int ls_i = part == kAll ? 0 : part == kFront ? 1 : 2;
     const LaneSet set = {pl->lanes3[ls_i], pl->fork3[ls_i], pl->join3[ls_i]};
@@ -308,7 +316,9 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
     // Profiling runs the chunks serially on the caller stream.
     auto fa = (FastRowsFwd)sel_fast_rows_fwd(pl->g.format, pl->t1_tma);
     const int nl = (rec || whole) ? 1 : pl->lanes;
-    if (!rec) {
+    // one whole-batch chunk runs on the caller's stream: no fork / join
+    const bool direct = rec || whole;
+    if (!direct) {
       cudaEventRecord(set.fork, st);
       for (int l = 0; l < nl; ++l) cudaStreamWaitEvent(set.lane[l], set.fork, 0);
     }
@@ -316,7 +326,7 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
     for (int b0 = 0; b0 < B; b0 += chunk, ++c) {
       const int nb = B - b0 < chunk ? B - b0 : chunk;
       const int l = whole ? 0 : c % pl->lanes;   // the lane's T1 / T2 buffers
-      const cudaStream_t ls = rec ? st : set.lane[c % nl];
+      const cudaStream_t ls = direct ? st : set.lane[c % nl];
       KParams kl = kp;
       kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_t1);
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_t2);
@@ -328,16 +338,25 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
       if (back && pl->fused_bc) {
         k448_colsinv<true><<<dim3(kClusterBC, nb), 32 * kWarpsBC, kSmemBC, ls>>>(kl, b0);
         if (rec) rec->mark(st, 1);
-      } else if (back) {
-        auto fb = (void (*)(KParams, int, CUtensorMap))pl->fnB;
-        fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm2[l]);
+      } else if (back && pl->flow_bc && do_b && do_c) {
+        auto ff = (void (*)(KParams, int, int, int, int, CUtensorMap))pl->fnF;
+        ff<<<(nb + pl->flow_lag) * (kNCB448 + kNRG448), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, nb, pl->flow_lag, l,
+                                                                                         tm2[l]);
         if (rec) rec->mark(st, 1);
-        auto fc = (void (*)(KParams, int))pl->fnC;
-        fc<<<dim3(kNRG448 / pl->kc_ppw, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
-        if (rec) rec->mark(st, 2);
+      } else if (back) {
+        if (do_b) {
+          auto fb = (void (*)(KParams, int, CUtensorMap))pl->fnB;
+          fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm2[l]);
+          if (rec) rec->mark(st, 1);
+        }
+        if (do_c) {
+          auto fc = (void (*)(KParams, int))pl->fnC;
+          fc<<<dim3(kNRG448 / pl->kc_ppw, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
+          if (rec) rec->mark(st, 2);
+        }
       }
     }
-    if (!rec) {
+    if (!direct) {
       for (int l = 0; l < nl; ++l) {
         cudaEventRecord(set.join[l], set.lane[l]);
         cudaStreamWaitEvent(st, set.join[l], 0);
@@ -351,16 +370,18 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
       if (rec) rec->mark(st, 0);
       launch_rank(pl, cfg, kp, 0, B, st, part == kAll && !rec, rec);
     }
-    if (back) {
+    if (do_b) {
       auto fb = (void (*)(KParams))sel_cols(pl->kh);
       fb<<<dim3(kp.NCB, B), blk, pl->smemB, st>>>(kp);
       if (rec) rec->mark(st, 1);
+    }
+    if (do_c) {
       auto fc = (void (*)(KParams))sel_rows_inv(pl->kw);
       fc<<<dim3(kp.NRG, B), blk, pl->smemC, st>>>(kp);
       if (rec) rec->mark(st, 2);
     }
   }
-  if (!back) return FC_OK;
+  if (!back || part == kCols) return FC_OK;
   if (part == kAll && !rec) {  // K_D waits for the K_D1 branch
     cudaEventRecord(pl->ev_aux, pl->aux);
     cudaStreamWaitEvent(st, pl->ev_aux, 0);
@@ -493,6 +514,8 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
   pl->off_estats = off;
   pl->slot_estats = align_up(B * 4 * sizeof(double));
   off += 2 * pl->slot_estats;
+  pl->off_flow = off;   // zero-initialised with the workspace; every flow launch re-arms it
+  off = align_up(off + ((size_t)kMaxFlowLanes * kFlowTicketStride + 2 * B) * sizeof(int));
   pl->ws_bytes = off;
   pl->state_hdr_bytes = align_up(B * sizeof(StreamHdr));
   pl->state_bytes = pl->state_hdr_bytes + align_up(specElems * sizeof(float2));
@@ -569,6 +592,14 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
       if (rc == FC_OK) rc = set_smem(pl->fnB, pl->smemB);
       if (rc == FC_OK) rc = set_smem(pl->fnC, pl->smemC);
       if (rc == FC_OK && pl->fused_bc) rc = set_smem((void*)k448_colsinv<true>, kSmemBC);
+      // K_B + K_C flow kernel (FC_BC_FLOW=1; FC_BC_LAG streams of lag,
+      // FC_BC_DISCARD=0 keeps the T2 lines in L2 after use)
+      pl->flow_bc = env_int("FC_BC_FLOW", 0, 0, 1) && pl->t2_tma && !pl->fused_bc && pl->kc_ppw == 1;
+      pl->flow_lag = env_int("FC_BC_LAG", 8, 1, 256);
+      if (pl->flow_bc) {
+        pl->fnF = env_int("FC_BC_DISCARD", 1, 0, 1) ? (void*)k448_bc_flow<6, true> : (void*)k448_bc_flow<6, false>;
+        if (rc == FC_OK) rc = set_smem(pl->fnF, pl->smemB);
+      }
     } else {
       rc = set_smem(sel_rows_fwd(pl->kw), pl->smemA);
       if (rc == FC_OK) rc = set_smem(sel_cols(pl->kh), pl->smemB);
@@ -619,7 +650,7 @@ int fc_plan_tokens(const fc_plan* pl) { return pl ? pl->kp.N : -1; }
 int fc_plan_launches(const fc_plan* pl) {
   if (!pl) return -1;
   // fast: K_A, K_D1, K_B, K_C (or K_BC) per chunk + K_D; generic: the five kernels once
-  return pl->fast ? (pl->fused_bc ? 3 : 4) * ((pl->g.batch + pl->chunk - 1) / pl->chunk) + 1 : 5;
+  return pl->fast ? (pl->fused_bc || pl->flow_bc ? 3 : 4) * ((pl->g.batch + pl->chunk - 1) / pl->chunk) + 1 : 5;
 }
 
 int fc_state_reset(const fc_plan* pl, void* state, int32_t first, int32_t count, void* stream) {
@@ -667,7 +698,11 @@ int fc_select_back(const fc_plan* pl, const fc_config* cfg, void* state, void* w
   if (rc != FC_OK) return rc;
   if (!split_ok(pl)) return FC_EUNSUPPORTED;
   const KParams kp = bind(pl, state, ws, out->energy, slot);
-  const int lrc = launch_select(pl, *cfg, nullptr, kp, *out, as_stream(stream), nullptr, kBack);
+  // timing probe only (scripts/): FC_PROBE_BACK_PART=cols|tail launches one
+  // half of the back (no ordering of the shared T2 / sums: results invalid)
+  const char* pp = getenv("FC_PROBE_BACK_PART");
+  const Part part = !pp ? kBack : !strcmp(pp, "cols") ? kCols : !strcmp(pp, "tail") ? kTail : kBack;
+  const int lrc = launch_select(pl, *cfg, nullptr, kp, *out, as_stream(stream), nullptr, part);
   if (lrc != FC_OK) return lrc;
   return launch_check();
 }

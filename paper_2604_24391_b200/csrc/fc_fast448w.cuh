@@ -59,15 +59,24 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 // unpacked with bins k and 448 - k of the same column.
 // TMST: T2 leaves through one TMA tensor store per CTA (the tile's swizzle is
 // the tensor map's 64-byte swizzle) instead of a copy loop over the threads.
-template <int MINB, bool LAZY, bool TMST>
-__global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int b0,
-                                                               const __grid_constant__ CUtensorMap tmT2) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[kWarpsB][2];
-  __shared__ double red[kWarpsB][4];
+// Static shared memory of one K_B item (per-warp mbarriers, warp partial sums).
+struct ColsSh {
+  uint64_t bar[kWarpsB][2];
+  double red[kWarpsB][4];
+};
+
+// One K_B work item: column group cx of stream b0 + bl.  FLOW: the item runs
+// inside k448_bc_flow; thread 0 commits the T2 tensor store and returns
+// without waiting for it (the flow loop publishes it later, see there).
+// Returns false for a cold stream (no T2 written).
+template <bool LAZY, bool TMST, bool FLOW>
+__device__ __forceinline__ bool cols_item(const KParams& kp, int b0, int cx, int bl, const CUtensorMap* tmT2,
+                                          unsigned char* smem, ColsSh& sh) {
+  auto& bar = sh.bar;
+  auto& red = sh.red;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bl = blockIdx.y, b = b0 + bl;
-  const int q = blockIdx.x * kWarpsB + wid;
+  const int b = b0 + bl;
+  const int q = cx * kWarpsB + wid;
   // [slot 0..3 (T1 column / FFT scratch) | prev 0..3 (state); later the T2 tile]
   float2* slot = reinterpret_cast<float2*>(smem + wid * (kSlotB * 8));
   float4* prev = reinterpret_cast<float4*>(smem + kWarpsB * kSlotB * 8 + wid * (kStCol * 16));
@@ -102,7 +111,7 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
         stg[st_idx(h, i, lane)] = make_float4(v[h][2 * i].x, v[h][2 * i].y, v[h][2 * i + 1].x, v[h][2 * i + 1].y);
     }
   }
-  if (!valid) return;  // cold stream: spectrum established (block-uniform)
+  if (!valid) return false;  // cold stream: spectrum established (block-uniform)
 
   // Per-lane sums of one column; the Hermitian weight (2, or 1 for the
   // packed DC / Nyquist column, warp-uniform) and ln 2 are applied once at the
@@ -207,25 +216,35 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
     double acc4 = 0.0;
 #pragma unroll
     for (int w = 0; w < kWarpsB; ++w) acc4 += red[w][threadIdx.x];
-    kp.stats[((size_t)b * kNCB448 + blockIdx.x) * 4 + threadIdx.x] = acc4;
+    kp.stats[((size_t)b * kNCB448 + cx) * 4 + threadIdx.x] = acc4;
   }
   if constexpr (TMST) {
     tma::fence_async_shared();
     __syncthreads();
     if (threadIdx.x == 0) {
       // box = 4 columns (64 bytes) x 224 row pairs of this stream's T2 block
-      tma::tensor_store_2d(&tmT2, tile, blockIdx.x * kWarpsB * 4, bl * 224);
-      tma::bulk_wait_read0();  // the tile must stay until the engine has read it
+      tma::tensor_store_2d(tmT2, tile, cx * kWarpsB * 4, bl * 224);
+      if constexpr (!FLOW) tma::bulk_wait_read0();  // the tile must stay until the engine has read it
     }
   } else {
+    static_assert(!FLOW, "the flow kernel writes T2 by tensor store");
     __syncthreads();
     const float4* t4 = reinterpret_cast<const float4*>(tile);
-    float4* T2 = reinterpret_cast<float4*>(kp.T2) + (size_t)bl * 224 * 224 + blockIdx.x * kWarpsB;
+    float4* T2 = reinterpret_cast<float4*>(kp.T2) + (size_t)bl * 224 * 224 + cx * kWarpsB;
     for (int u = threadIdx.x; u < 224 * 4; u += 32 * kWarpsB) {
       const int pr = u >> 2, col = (u & 3) ^ ((pr >> 1) & 3);
       T2[(size_t)pr * 224 + col] = t4[u];
     }
   }
+  return true;
+}
+
+template <int MINB, bool LAZY, bool TMST>
+__global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int b0,
+                                                               const __grid_constant__ CUtensorMap tmT2) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ ColsSh sh;
+  cols_item<LAZY, TMST, false>(kp, b0, blockIdx.x, blockIdx.y, &tmT2, smem, sh);
 }
 
 // ------------------------------------------------------------- K_C 448 ----
@@ -236,21 +255,51 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
 // per CTA (224 / (kWarpsC PPW) per stream), merged by K_D in its fixed tie
 // order.  With PPW = 2 a warp's two blocks arrive in one bulk-copy phase and
 // its twiddles, gather indices and reductions serve both pairs.
-template <int MINB, bool LAZY, int PPW = 1>
-__global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, int b0) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ PeakKey redk[kWarpsC];
-  __shared__ float redv[kWarpsC];
-  __shared__ __align__(8) uint64_t barc[kWarpsC];
+// Static shared memory of one K_C item.
+struct RowsInvSh {
+  PeakKey redk[kWarpsC];
+  float redv[kWarpsC];
+  uint64_t barc[kWarpsC];
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One K_C work item: row-pair group cx of stream b0 + bl.  FLOW: waits until
+// all kNCB448 K_B items of the stream have published their T2 tiles (the last
+// K_C item of the stream re-arms the counters for the next launch).  DISCARD:
+// the T2 lines the item has staged are dropped from L2 without a write-back
+// (each 3.5 KB block is read by exactly one warp, and the next step's K_B
+// rewrites it whole).
+template <bool LAZY, int PPW, bool FLOW, bool DISCARD>
+__device__ __forceinline__ void rows_inv_item(const KParams& kp, int b0, int cx, int bl, unsigned char* smem,
+                                              RowsInvSh& sh, int* done, int* consumed) {
+  auto& redk = sh.redk;
+  auto& redv = sh.redv;
+  auto& barc = sh.barc;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bl = blockIdx.y, b = b0 + bl;
+  const int b = b0 + bl;
   if (kp.hdr[b].valid == 0) return;  // cold stream (block-uniform)
-  const int pair0 = (blockIdx.x * kWarpsC + wid) * PPW;
+  if constexpr (FLOW) {
+    if (threadIdx.x == 0) {
+      while (ld_acquire_gpu(done + b) < kNCB448) __nanosleep(128);
+      if (atomicAdd(consumed + b, 1) == kNRG448 / PPW - 1) {
+        done[b] = 0;
+        consumed[b] = 0;
+      }
+    }
+    __syncthreads();
+  }
+  const int pair0 = (cx * kWarpsC + wid) * PPW;
   float2* S0 = reinterpret_cast<float2*>(smem) + wid * PPW * w448::XS;
   const float4* T2 = reinterpret_cast<const float4*>(kp.T2) + ((size_t)bl * 224 + pair0) * 224;
   // each row pair's 3.5 KB T2 block lands in its own FFT scratch region with
   // one bulk copy; the lanes then gather their (mirrored) columns from there
   if (lane == 0) {
+    if constexpr (FLOW) asm volatile("fence.proxy.async.global;" ::: "memory");
     tma::bar_init(&barc[wid], 1);
     tma::bar_expect(&barc[wid], PPW * 224 * 16);
 #pragma unroll
@@ -260,6 +309,11 @@ __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, 
   tw.load(kp.tw448, kp.tw64, lane);
   __syncwarp();
   tma::bar_wait(&barc[wid], 0);
+  if constexpr (DISCARD) {
+    // 28 lines of 128 bytes per 3.5 KB block
+    if (lane < 28 * PPW)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<const char*>(T2) + 128 * lane) : "memory");
+  }
   const int k1a = lane >> 3, j1 = lane & 7;
   PeakKey best = {-CUDART_INF_F, 0x7fffffff, 0x7fffffff};
   float v2 = -CUDART_INF_F;
@@ -354,6 +408,65 @@ __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, 
     }
     PeakPart pp;
     pp.v = best.v; pp.v2 = v2; pp.y = best.pos / 448; pp.j = best.pos % 448;
-    kp.peaks[(size_t)b * (kNRG448 / PPW) + blockIdx.x] = pp;
+    kp.peaks[(size_t)b * (kNRG448 / PPW) + cx] = pp;
+  }
+}
+
+template <int MINB, bool LAZY, int PPW = 1, bool DISCARD = false>
+__global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, int b0) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ RowsInvSh sh;
+  rows_inv_item<LAZY, PPW, false, DISCARD>(kp, b0, blockIdx.x, blockIdx.y, smem, sh, nullptr, nullptr);
+}
+
+// ------------------------------------------------------- K_B + K_C flow ----
+// K_B and K_C as one launch of work items taken in ticket order (FC_BC_FLOW=1,
+// an option: measured slower than the two kernels): round r holds
+// the kNCB448 K_B items of stream r, then the kNRG448 K_C items of stream
+// r - lag.  A K_C item waits (spinning) for its stream's K_B items; those hold
+// smaller tickets, and a CTA draws one ticket and processes it at once, so
+// they are running or done — the wait cannot deadlock.  (A persistent variant
+// that prefetched its next ticket broke exactly this: a drawn but unstarted
+// K_B item behind a waiting K_C item, and two such CTAs deadlocked.)  T2 of
+// the last `lag` streams is still in L2 when K_C reads it, and K_C discards
+// what it has read (DISCARD), so T2 costs neither its DRAM read nor its
+// write-back.  flow = [kMaxFlowLanes tickets (128 B apart) | done[B] |
+// consumed[B]], zero-initialised; each launch re-arms what it used.
+constexpr int kFlowTicketStride = 32;   // ints
+constexpr int kMaxFlowLanes = 8;
+
+template <int MINB, bool DISCARD>
+__global__ void __launch_bounds__(32 * kWarpsB, MINB)
+    k448_bc_flow(const __grid_constant__ KParams kp, int b0, int nb, int lag, int lane_id,
+                 const __grid_constant__ CUtensorMap tmT2) {
+  static_assert(kWarpsB == kWarpsC, "one CTA shape for both item kinds");
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ ColsSh shb;
+  __shared__ RowsInvSh shc;
+  __shared__ int tk;
+  int* ticket = kp.flow + lane_id * kFlowTicketStride;
+  int* done = kp.flow + kMaxFlowLanes * kFlowTicketStride;
+  int* consumed = done + kp.B;
+  if (threadIdx.x == 0) {
+    const int t = atomicAdd(ticket, 1);
+    if (t == (int)gridDim.x - 1) *ticket = 0;   // every ticket is taken: re-arm
+    tk = t;
+  }
+  __syncthreads();
+  constexpr int per = kNCB448 + kNRG448;
+  const int r = tk / per, w = tk - r * per;
+  if (w < kNCB448) {
+    if (r < nb && cols_item<true, true, true>(kp, b0, w, r, &tmT2, smem, shb) && threadIdx.x == 0) {
+      // the tile is in global memory (async proxy) before the generic-proxy
+      // release that lets this stream's K_C items load it
+      tma::bulk_wait0();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      atomicAdd(done + b0 + r, 1);
+    }
+  } else {
+    const int sidx = r - lag;
+    if (sidx >= 0 && sidx < nb)
+      rows_inv_item<true, 1, true, DISCARD>(kp, b0, w - kNCB448, sidx, smem, shc, done, consumed);
   }
 }

@@ -77,6 +77,7 @@ struct KParams {
   int16_t* order;   // [B][N] all tokens ascending (E, index) (K_D1 -> K_D)
   uint8_t* freshm;  // [B][N] refresh mask (K_D1 -> K_D)
   double* estats;   // [B][4] mean, std, threshold, refresh count (K_D1 -> K_D)
+  int* flow;        // fast path, K_B + K_C flow kernel: tickets and per-stream counters
 };
 
 // --------------------------------------------------------------- helpers --

@@ -36,11 +36,25 @@ fs = torch.cuda.Stream()
 side = torch.cuda.Stream(priority=-1)
 
 
-def make(t, front, back, splice, whole=False):
+bs2 = torch.cuda.Stream()
+
+
+def make(t, front, back, splice, whole=False, deep=False):
     def fn():
         cur = torch.cuda.current_stream()
         fs.wait_stream(cur)
         side.wait_stream(cur)
+        bs2.wait_stream(cur)
+        if deep:
+            # timing only: K_B of step t + 1 beside K_C + K_D of step t (the
+            # probe env launches one half of the back; T2 / sums unordered)
+            with torch.cuda.stream(bs2):
+                os.environ["FC_PROBE_BACK_PART"] = "cols"
+                eng.select_back(cfg, outs[(t + 1) & 1], (t + 1) & 1, refresh_shift=1)
+            os.environ["FC_PROBE_BACK_PART"] = "tail"
+            eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=1)
+            del os.environ["FC_PROBE_BACK_PART"]
+            cur.wait_stream(bs2)
         if whole:
             eng.select(frames[t % R], cfg, out=outs[t & 1], refresh_shift=1)
         if front:
@@ -56,12 +70,12 @@ def make(t, front, back, splice, whole=False):
     return fn
 
 
-def timeit(label, front, back, splice, whole=False, n=64):
+def timeit(label, front, back, splice, whole=False, n=64, deep=False):
     base_k = spl.k
     graphs = []
     for p in range(R):
         spl.k = (base_k + p) & 1
-        graphs.append(StepGraph(make(p + 1, front, back, splice, whole)))
+        graphs.append(StepGraph(make(p + 1, front, back, splice, whole, deep)))
     spl.k = base_k
     for i in range(R):
         graphs[i].replay()
@@ -82,6 +96,8 @@ timeit("back (K_B + K_C + K_D)", False, True, False)
 timeit("front + back", True, True, False)
 timeit("splice", False, False, True)
 timeit("front + back + splice", True, True, True)
+timeit("deep: front+cols+tail+splice", True, False, True, deep=True)
+timeit("deep: cols + tail", False, False, False, deep=True)
 timeit("whole select", False, False, False, whole=True)
 timeit("whole select + splice", False, False, True, whole=True)
 prof = []

@@ -550,6 +550,50 @@ def test_fused_cluster_colsinv_matches_split_kernels(cuda, monkeypatch, streams)
     assert rep.ok, rep.errors
 
 
+@pytest.mark.parametrize("streams,lag,discard", [(40, 8, "1"), (3, 1, "1"), (20, 64, "0"), (200, 4, "1")])
+def test_flow_colsinv_matches_split_kernels(cuda, monkeypatch, streams, lag, discard):
+    """The K_B + K_C flow kernel (FC_BC_FLOW=1: one launch of ticket-ordered
+    work items, K_C items of a stream waiting for its K_B items, T2 read from
+    L2 and discarded) runs the same items as K_B -> T2 -> K_C: every output and
+    the spectrum state bit-identical, through fc_select (small batches: two
+    concurrent half-batch launches with their own tickets) and the split-phase
+    front / back, over cold starts, a reset stream and repeated launches (the
+    counters re-arm)."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    T = 5
+    frames = torch_stream_frames(streams, T, 448, 448, seed=37, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    monkeypatch.setenv("FC_BC_FLOW", "0")
+    ref = fc.FreqCacheEngine(streams, 448, 448, 14, fmt="rgb")
+    monkeypatch.setenv("FC_BC_FLOW", "1")
+    monkeypatch.setenv("FC_BC_LAG", str(lag))
+    monkeypatch.setenv("FC_BC_DISCARD", discard)
+    flow = fc.FreqCacheEngine(streams, 448, 448, 14, fmt="rgb")
+    chunks = (ref.launches_per_select - 1) // 4
+    assert flow.launches_per_select == ref.launches_per_select - chunks
+    outs = [flow.new_output(), flow.new_output()]
+
+    def same(a, b, t):
+        for name in ("reuse_idx", "recompute_idx", "src_map", "reuse_mask", "refresh_mask", "energy", "results"):
+            assert torch.equal(getattr(a, name), getattr(b, name)), (t, name)
+
+    for t in range(T):
+        if t == 3:
+            ref.reset(streams // 2, 1)
+            flow.reset(streams // 2, 1)
+        a = ref.select(frames[t], cfg, refresh_shift=1)
+        if t % 2 == 0:
+            b = flow.select(frames[t], cfg, refresh_shift=1)
+        else:
+            b = outs[t & 1]
+            flow.select_front(frames[t], cfg, b, t & 1, refresh_shift=1)
+            flow.select_back(cfg, b, t & 1, refresh_shift=1)
+        same(a, b, t)
+        assert torch.equal(ref.state, flow.state), t
+
+
 def test_gather_patches_matches_torch_patchify(cuda):
     """fc_gather_patches (config 4's recomputed-token pixels, straight from
     fp32 RGB frames to bf16) equals torch's patchify + cast + row gather bit
