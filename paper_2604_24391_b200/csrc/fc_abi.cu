@@ -63,6 +63,8 @@ struct fc_plan {
   bool flow_bc = false;                // K_B + K_C as one ticket-ordered flow kernel (T2 through L2)
   int flow_lag = 8;                    // flow: streams K_C trails K_B by
   void* fnF = nullptr;
+  bool pdl = false;                     // K_C / K_D of the back as programmatic dependents (FC_PDL=1)
+  int probe_skip = 0;                  // timing probes only (FC_PROBE_SKIP bitmask): kernels not launched
   size_t off_flow = 0;
   int kc_ppw = 1;                      // K_C row pairs per warp
   void* fnC = nullptr;
@@ -257,8 +259,12 @@ void launch_rank(const fc_plan* pl, const fc_config& cfg, const KParams& kp, int
     cudaStreamWaitEvent(pl->aux, pl->ev_a, 0);
     rs = pl->aux;
   }
-  if (nb <= kSmallBatch) k_rank<512><<<nb, 512, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
-  else k_rank<FC_SEL_THREADS><<<nb, FC_SEL_THREADS, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
+  if (pl->probe_skip & 2) {
+  } else if (nb <= kSmallBatch) {
+    k_rank<512><<<nb, 512, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
+  } else {
+    k_rank<FC_SEL_THREADS><<<nb, FC_SEL_THREADS, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
+  }
   if (rec) rec->mark(after, 4);
 }
 
@@ -266,6 +272,28 @@ void launch_rank(const fc_plan* pl, const fc_config& cfg, const KParams& kp, int
 // reads them: each chunk needs its own T1 buffers (chunks <= lanes).
 bool split_ok(const fc_plan* pl) {
   return !pl->fast || (pl->g.batch + pl->chunk - 1) / pl->chunk <= pl->lanes;
+}
+
+// Launch `k` on `st`, as a programmatic dependent of the previous kernel on
+// the stream when `pdl` (the kernel waits with griddepcontrol.wait before it
+// reads its predecessor's outputs).
+template <typename... P, typename... A>
+void launch_maybe_pdl(bool pdl, void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... args) {
+  if (!pdl) {
+    k<<<grid, block, smem, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaLaunchKernelEx(&lc, k, static_cast<P>(args)...);
 }
 
 // Which kernels a call launches: the whole select, or one half of the
@@ -331,7 +359,8 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
       kl.T = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T) + l * pl->lane_t1);
       kl.T2 = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(kp.T2) + l * pl->lane_t2);
       if (front) {
-        fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1, tm1[l]);
+        if (!(pl->probe_skip & 1))
+          fa<<<dim3(32, nb), kThreadsA448, pl->smemA, ls>>>(kl, pl->dct14, frames, b0, 1, tm1[l]);
         if (rec) rec->mark(st, 0);
         launch_rank(pl, cfg, kp, b0, nb, ls, part == kAll && !rec, rec);
       }
@@ -344,14 +373,15 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
                                                                                          tm2[l]);
         if (rec) rec->mark(st, 1);
       } else if (back) {
-        if (do_b) {
+        if (do_b && !(pl->probe_skip & 4)) {
           auto fb = (void (*)(KParams, int, CUtensorMap))pl->fnB;
           fb<<<dim3(kNCB448, nb), 32 * kWarpsB, pl->smemB, ls>>>(kl, b0, tm2[l]);
           if (rec) rec->mark(st, 1);
         }
-        if (do_c) {
+        if (do_c && !(pl->probe_skip & 8)) {
           auto fc = (void (*)(KParams, int))pl->fnC;
-          fc<<<dim3(kNRG448 / pl->kc_ppw, nb), 32 * kWarpsC, pl->smemC, ls>>>(kl, b0);
+          launch_maybe_pdl(pl->pdl && part == kBack && do_b && !rec, fc, dim3(kNRG448 / pl->kc_ppw, nb),
+                           dim3(32 * kWarpsC), pl->smemC, ls, kl, b0);
           if (rec) rec->mark(st, 2);
         }
       }
@@ -390,9 +420,17 @@ int launch_select(const fc_plan* pl, const fc_config& cfg, const void* frames, c
   // stream more threads there (FC_SEL_NT overrides)
   static const int nt_env = env_int("FC_SEL_NT", 0, 0, 1024);
   const int nt = nt_env ? nt_env : (B <= 128 ? 512 : FC_SEL_THREADS);
-  if (nt >= 1024) k_select<1024><<<B, 1024, pl->smemD, st>>>(kp, cfg, out);
-  else if (nt >= 512) k_select<512><<<B, 512, pl->smemD, st>>>(kp, cfg, out);
-  else k_select<FC_SEL_THREADS><<<B, FC_SEL_THREADS, pl->smemD, st>>>(kp, cfg, out);
+  // PDL only where K_D directly follows K_C on the caller's stream
+  const bool pdl_d = pl->pdl && pl->fast && part == kBack && !rec && !pl->fused_bc && !pl->flow_bc &&
+                     !(pl->probe_skip & 8);
+  if (pl->probe_skip & 16) {
+  } else if (nt >= 1024) {
+    launch_maybe_pdl(pdl_d, k_select<1024>, dim3(B), dim3(1024), pl->smemD, st, kp, cfg, out);
+  } else if (nt >= 512) {
+    launch_maybe_pdl(pdl_d, k_select<512>, dim3(B), dim3(512), pl->smemD, st, kp, cfg, out);
+  } else {
+    launch_maybe_pdl(pdl_d, k_select<FC_SEL_THREADS>, dim3(B), dim3(FC_SEL_THREADS), pl->smemD, st, kp, cfg, out);
+  }
   if (rec) rec->mark(st, 3);
   return FC_OK;
 }
@@ -596,6 +634,10 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
       // FC_BC_DISCARD=0 keeps the T2 lines in L2 after use)
       pl->flow_bc = env_int("FC_BC_FLOW", 0, 0, 1) && pl->t2_tma && !pl->fused_bc && pl->kc_ppw == 1;
       pl->flow_lag = env_int("FC_BC_LAG", 8, 1, 256);
+      // timing probes (scripts/skip_probe.sh): 1 K_A, 2 K_D1, 4 K_B, 8 K_C,
+      // 16 K_D are not launched — results are invalid
+      pl->probe_skip = env_int("FC_PROBE_SKIP", 0, 0, 31);
+      pl->pdl = env_int("FC_PDL", 0, 0, 1) != 0;
       if (pl->flow_bc) {
         pl->fnF = env_int("FC_BC_DISCARD", 1, 0, 1) ? (void*)k448_bc_flow<6, true> : (void*)k448_bc_flow<6, false>;
         if (rc == FC_OK) rc = set_smem(pl->fnF, pl->smemB);

@@ -244,6 +244,9 @@ __global__ void __launch_bounds__(32 * kWarpsB, MINB) k448_cols(KParams kp, int 
                                                                const __grid_constant__ CUtensorMap tmT2) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ ColsSh sh;
+  // FC_PDL=1: K_C may be scheduled once every K_B CTA has started (it waits
+  // for K_B's completion before reading T2); a no-op otherwise
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   cols_item<LAZY, TMST, false>(kp, b0, blockIdx.x, blockIdx.y, &tmT2, smem, sh);
 }
 
@@ -274,7 +277,7 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 // the T2 lines the item has staged are dropped from L2 without a write-back
 // (each 3.5 KB block is read by exactly one warp, and the next step's K_B
 // rewrites it whole).
-template <bool LAZY, int PPW, bool FLOW, bool DISCARD>
+template <bool LAZY, int PPW, bool FLOW, bool DISCARD, bool PDL = false>
 __device__ __forceinline__ void rows_inv_item(const KParams& kp, int b0, int cx, int bl, unsigned char* smem,
                                               RowsInvSh& sh, int* done, int* consumed) {
   auto& redk = sh.redk;
@@ -293,6 +296,9 @@ __device__ __forceinline__ void rows_inv_item(const KParams& kp, int b0, int cx,
     }
     __syncthreads();
   }
+  // launched as a programmatic dependent of K_B (FC_PDL=1): T2 is complete
+  // and visible after this (a no-op for a plain launch)
+  if constexpr (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int pair0 = (cx * kWarpsC + wid) * PPW;
   float2* S0 = reinterpret_cast<float2*>(smem) + wid * PPW * w448::XS;
   const float4* T2 = reinterpret_cast<const float4*>(kp.T2) + ((size_t)bl * 224 + pair0) * 224;
@@ -322,14 +328,18 @@ __device__ __forceinline__ void rows_inv_item(const KParams& kp, int b0, int cx,
     const int ya = 2 * (pair0 + it);
     float2* S = S0 + it * w448::XS;
     const float4* Sb = reinterpret_cast<const float4*>(S);
+    // bin k = kk + 56 j2 with kk = k1a + 4 h + 7 j1 in [0, 55], so k < 224
+    // exactly when j2 < 4 (compile time); the packed DC / Nyquist column (k = 0
+    // and k = 224) belongs to lane 0 of half 0 at j2 = 0 and j2 = 4
+    const int kk = k1a + 7 * j1;
     float4 in[2][8];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (h == 0 || lane < 24) {
 #pragma unroll
         for (int j2 = 0; j2 < 8; ++j2) {
-          const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
-          const int qq = (k == 0 || k == 224) ? 0 : (k < 224 ? k : 448 - k);
+          const int k = kk + 4 * h + 56 * j2;
+          const int qq = j2 < 4 ? k : (h == 0 && j2 == 4 && lane == 0 ? 0 : 448 - k);
           in[h][j2] = Sb[qq];
         }
       }
@@ -341,13 +351,11 @@ __device__ __forceinline__ void rows_inv_item(const KParams& kp, int b0, int cx,
       if (h == 0 || lane < 24) {
 #pragma unroll
         for (int j2 = 0; j2 < 8; ++j2) {
-          const int k = k1a + 4 * h + 7 * j1 + 56 * j2;
           const float4 t = in[h][j2];  // (A = row ya, B = row ya + 1) at the column
-          float2 z;
-          if (k == 0) z = make_float2(t.x, t.z);
-          else if (k == 224) z = make_float2(t.y, t.w);
-          else if (k < 224) z = make_float2(t.x - t.w, t.y + t.z);   // G_a + i G_b
-          else z = make_float2(t.x + t.w, t.z - t.y);                // conj G_a + i conj G_b
+          float2 z = j2 < 4 ? make_float2(t.x - t.w, t.y + t.z)     // G_a + i G_b
+                            : make_float2(t.x + t.w, t.z - t.y);    // conj G_a + i conj G_b
+          if (h == 0 && j2 == 0 && lane == 0) z = make_float2(t.x, t.z);   // k = 0
+          if (h == 0 && j2 == 4 && lane == 0) z = make_float2(t.y, t.w);   // k = 224
           v[h][j2] = z;
         }
       }
@@ -416,7 +424,8 @@ template <int MINB, bool LAZY, int PPW = 1, bool DISCARD = false>
 __global__ void __launch_bounds__(32 * kWarpsC, MINB) k448_rows_inv(KParams kp, int b0) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ RowsInvSh sh;
-  rows_inv_item<LAZY, PPW, false, DISCARD>(kp, b0, blockIdx.x, blockIdx.y, smem, sh, nullptr, nullptr);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // FC_PDL=1: K_D may be scheduled
+  rows_inv_item<LAZY, PPW, false, DISCARD, true>(kp, b0, blockIdx.x, blockIdx.y, smem, sh, nullptr, nullptr);
 }
 
 // ------------------------------------------------------- K_B + K_C flow ----

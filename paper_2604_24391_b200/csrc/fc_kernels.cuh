@@ -764,6 +764,9 @@ __global__ void __launch_bounds__(NT) k_rank(KParams kp, double lam, int b0) {
 template <int NT>
 __global__ void __launch_bounds__(NT) k_select(KParams kp, fc_config cfg, fc_select_out out) {
   extern __shared__ __align__(128) unsigned char smem[];
+  // launched as a programmatic dependent of K_C (FC_PDL=1): K_C's partials
+  // are complete and visible after this (a no-op for a plain launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int b = blockIdx.x;
   const int N = kp.N;
   int* ki = reinterpret_cast<int*>(smem);                 // N: reuse list

@@ -70,7 +70,12 @@ def make(t, front, back, splice, whole=False, deep=False):
     return fn
 
 
+ONLY = os.environ.get("PROBE_ONLY")
+
+
 def timeit(label, front, back, splice, whole=False, n=64, deep=False):
+    if ONLY and label.strip() != ONLY:
+        return None
     base_k = spl.k
     graphs = []
     for p in range(R):
@@ -101,5 +106,7 @@ timeit("deep: cols + tail", False, False, False, deep=True)
 timeit("whole select", False, False, False, whole=True)
 timeit("whole select + splice", False, False, True, whole=True)
 prof = []
+if ONLY:
+    sys.exit(0)
 eng.select(frames[0], cfg, refresh_shift=1, profile=prof)
 print("serial kernels (rows_fwd, cols, rows_inv, K_D1+K_D):", ["%.1f" % (x * 1e3) for x in prof])

@@ -594,6 +594,38 @@ def test_flow_colsinv_matches_split_kernels(cuda, monkeypatch, streams, lag, dis
         assert torch.equal(ref.state, flow.state), t
 
 
+@pytest.mark.parametrize("streams", [64, 5])
+def test_pdl_back_matches_plain_launches(cuda, monkeypatch, streams):
+    """FC_PDL=1: K_C and K_D of the split-phase back launched as programmatic
+    dependents (scheduled while their predecessor drains, griddepcontrol.wait
+    before reading its outputs) give bit-identical outputs and state, also
+    when captured in a CUDA graph."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    T = 4
+    frames = torch_stream_frames(streams, T, 448, 448, seed=41, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    monkeypatch.setenv("FC_PDL", "0")
+    ref = fc.FreqCacheEngine(streams, 448, 448, 14, fmt="rgb")
+    monkeypatch.setenv("FC_PDL", "1")
+    pdl = fc.FreqCacheEngine(streams, 448, 448, 14, fmt="rgb")
+    oa = [ref.new_output(), ref.new_output()]
+    ob = [pdl.new_output(), pdl.new_output()]
+    for t in range(T):
+        for eng, o in ((ref, oa), (pdl, ob)):
+            eng.select_front(frames[t], cfg, o[t & 1], t & 1, refresh_shift=1)
+            if t == T - 1 and eng is pdl:
+                g = fc.StepGraph(lambda: eng.select_back(cfg, o[t & 1], t & 1, refresh_shift=1))
+                g.replay()
+            else:
+                eng.select_back(cfg, o[t & 1], t & 1, refresh_shift=1)
+        torch.cuda.synchronize()
+        for name in ("reuse_idx", "recompute_idx", "src_map", "reuse_mask", "refresh_mask", "energy", "results"):
+            assert torch.equal(getattr(oa[t & 1], name), getattr(ob[t & 1], name)), (t, name)
+        assert torch.equal(ref.state, pdl.state), t
+
+
 def test_gather_patches_matches_torch_patchify(cuda):
     """fc_gather_patches (config 4's recomputed-token pixels, straight from
     fp32 RGB frames to bf16) equals torch's patchify + cast + row gather bit
