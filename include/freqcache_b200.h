@@ -133,7 +133,11 @@ const char* fc_strerror(int code);
 int  fc_plan_create(const fc_geometry* geom, fc_plan** out);
 void fc_plan_destroy(fc_plan* plan);
 int64_t fc_plan_state_bytes(const fc_plan* plan);     /* per-stream state x B */
-int64_t fc_plan_workspace_bytes(const fc_plan* plan); /* scratch             */
+int64_t fc_plan_workspace_bytes(const fc_plan* plan); /* scratch; zero it once
+                                                          at allocation (the
+                                                          optional K_B + K_C
+                                                          flow kernel keeps its
+                                                          tickets there)       */
 int  fc_plan_tokens(const fc_plan* plan);             /* N = rows*cols        */
 int  fc_plan_launches(const fc_plan* plan);           /* kernels per fc_select */
 
