@@ -102,7 +102,9 @@ class Block(torch.nn.Module):
                    F.linear(y, self.qkv.weight, self.qkv.bias).split(d, dim=-1))
         if _flash_varlen is not None and x.dtype in (torch.float16, torch.bfloat16):
             cu = offsets.to(torch.int32)
-            o = _flash_varlen(q.contiguous(), k.contiguous(), v.contiguous(), cu, cu, max_len, max_len)
+            # q / k / v stay strided views of the QKV output (unit stride in
+            # the head dimension is all the kernel needs): no copies
+            o = _flash_varlen(q, k, v, cu, cu, max_len, max_len)
         else:
             def nj(t):
                 return torch.nested.nested_tensor_from_jagged(t, offsets).transpose(1, 2)
@@ -196,9 +198,16 @@ class CachedEncoder:
         # from a CUDA graph per (row bucket, cache buffer); its per-step inputs
         # are copied into static buffers first
         self.b0_graphs = {} if self.tail_graphs is not None else None
+        # subset with graphs: the whole packed encoder of a step is replayed
+        # from a CUDA graph per (row bucket, cache buffer) — 27 blocks of
+        # eager launches would leave the GPU waiting on the host
+        # (flash-attention varlen, bf16 / fp16, takes the zero-length and
+        # padding segments inside a graph; other dtypes run eagerly)
+        self.sub_graphs = ({} if (graphs and mode == "subset" and _flash_varlen is not None
+                                  and dt in (torch.float16, torch.bfloat16)) else None)
         nb = batch * n
         self.bucket = max(64, min(1024, -(-nb // 16 // 64) * 64))   # ~16 row buckets
-        if self.b0_graphs is not None:
+        if self.b0_graphs is not None or self.sub_graphs is not None:
             self.st_frames = torch.zeros((batch, c.image, c.image, 3), dtype=torch.float32, device=device)
             self.st_src = torch.zeros((batch, n), dtype=torch.int32, device=device)
             self.st_rec = torch.zeros((batch, n), dtype=torch.int32, device=device)
@@ -224,7 +233,7 @@ class CachedEncoder:
             with torch.no_grad():
                 for o in (0, 1):
                     self._tail(o)
-            self.prepare_graphs()
+        self.prepare_graphs()
 
     def _issue_select(self, frames, cfg, refresh_shift):
         """Select on the side stream (in stream order with every earlier
@@ -323,6 +332,15 @@ class CachedEncoder:
             y = self._tail(o)
             if marks is not None:
                 marks[-1][2].record(main)
+        elif self.sub_graphs is not None and total:
+            self.st_frames.copy_(frames)
+            self.st_src.copy_(out.src_map)
+            self.st_rec.copy_(out.recompute_idx)
+            self.st_offsets.copy_(offsets)
+            tp = -(-total // self.bucket) * self.bucket
+            self._subset_graph(tp, o).replay()
+            self._prefetch(next_frames, cfg, refresh_shift)
+            y = self.h1[o]
         else:
             # the whole packed encoder follows: the next select goes beside it
             self._prefetch(next_frames, cfg, refresh_shift)
@@ -378,6 +396,47 @@ class CachedEncoder:
         splice_packed(self.st_src, self.h1[i], self.ages[i], x1, offsets[:B], self.h1[o], self.ages[o],
                       status=self.status)
 
+    def _subset_static(self, tp, o):
+        """The subset step on the static buffers for tp (>= the step's
+        recomputed rows) packed rows: gathers, embedding, every block over
+        the packed rows (attention within each stream's segment; the rows
+        past the step's count form one extra segment of their own), final
+        LN, the splice into cache buffer o.  Padding rows compute throw-away
+        values that no splice reads."""
+        m, B = self.m, self.B
+        n = m.c.tokens
+        dt = next(m.parameters()).dtype
+        i = 1 - o
+        offsets = self.st_offsets
+        ar = torch.arange(tp, device=self.device)
+        sid = torch.searchsorted(offsets[1:], ar, right=True).clamp_(max=B - 1)
+        pos = (ar - offsets[sid]).clamp_(0, n - 1)
+        tok = self.st_rec.view(-1).index_select(0, sid * n + pos).long().clamp_(min=0)
+        flat = sid * n + tok
+        x = m.embed(self._embed_input(self.st_frames, flat, dt)) + m.pos.index_select(0, tok)
+        # segments: the B streams (empty ones have zero length), then padding
+        seg = torch.cat([offsets, torch.full((1,), tp, dtype=offsets.dtype, device=self.device)])
+        for blk in m.blocks:
+            x = blk.forward_packed(x, seg, max(n, self.bucket))
+        packed = m.ln(x)
+        splice_packed(self.st_src, self.h1[i], self.ages[i], packed, offsets[:B], self.h1[o], self.ages[o],
+                      status=self.status)
+
+    def _subset_graph(self, tp, o):
+        key = (tp, o)
+        g = self.sub_graphs.get(key)
+        if g is None:
+            st = torch.cuda.Stream(self.device)
+            st.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(st):          # warm-up outside capture (library plans)
+                self._subset_static(tp, o)
+            torch.cuda.current_stream(self.device).wait_stream(st)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=self._pool):
+                self._subset_static(tp, o)
+            self.sub_graphs[key] = g
+        return g
+
     def _embed_input(self, frames, flat, dt):
         """Patch pixels of the packed tokens: gathered straight from fp32 RGB
         frames in bf16 (``fc_gather_patches``), else through torch."""
@@ -404,15 +463,21 @@ class CachedEncoder:
         return g
 
     def prepare_graphs(self):
-        """Capture every block-0 bucket graph up front (no capture inside a
-        timed loop)."""
-        if self.b0_graphs is None:
+        """Capture every bucket graph up front (no capture inside a timed
+        loop); the caches hold no state yet, so the warm-up runs are
+        harmless."""
+        make = self._block0_graph if self.b0_graphs is not None else (
+            self._subset_graph if self.sub_graphs is not None else None)
+        if make is None:
             return
         with torch.no_grad():
             nb = self.B * self.m.c.tokens
             for tp in range(self.bucket, -(-nb // self.bucket) * self.bucket + 1, self.bucket):
                 for o in (0, 1):
-                    self._block0_graph(tp, o)
+                    make(tp, o)
+            self.h1.zero_()
+            self.ages.zero_()
+            self.status.zero_()
 
     def _tail(self, o):
         """Blocks 1.. and the final LN on every token of cache buffer o —

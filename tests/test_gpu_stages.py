@@ -397,6 +397,52 @@ def test_vit_layer1_step_matches_reference_semantics(cuda, dtype):
         enc.check()
 
 
+def test_vit_subset_step_matches_reference_semantics(cuda):
+    """subset mode (bf16: the packed encoder replayed from a CUDA graph per
+    row bucket, flash-attention varlen with zero-length and padding
+    segments) against a plain-torch restatement, stream by stream: the
+    recomputed tokens (row-major) run the whole encoder attending among
+    themselves; reused tokens take their displacement-mapped cached final
+    state.  Also equal to the eager (ungraphed) packed path."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.synth import torch_stream_frames
+    from paper_2604_24391_b200.vit import CachedEncoder, ViT, ViTConfig, cosine
+    c = ViTConfig(image=112, patch=14, width=64, mlp=128, heads=2, layers=3)
+    model = ViT(c).cuda().to(torch.bfloat16).eval()
+    T, B = 5, 3
+    frames = torch_stream_frames(B, T, 112, 112, seed=13, device="cuda")
+    cfg = fc.CacheConfig(patch_size=14)
+    enc = CachedEncoder(model, B, mode="subset")
+    assert enc.sub_graphs, "the bf16 subset path must be graphed"
+    eager = CachedEncoder(model, B, mode="subset", graphs=False)
+    with torch.no_grad():
+        hc = None
+        for t in range(T):
+            nxt = frames[t + 1] if t + 1 < T else None
+            y, out = enc.step(frames[t], cfg, next_frames=nxt)
+            ye, oute = eager.step(frames[t], cfg, next_frames=nxt)
+            assert torch.equal(out.src_map, oute.src_map)
+            assert float(cosine(y, ye).min()) > 0.9999, t
+            x0 = model.embed_tokens(model.patches(frames[t].to(torch.bfloat16)))
+            sm = out.src_map.long()
+            h = torch.empty_like(x0)
+            for b in range(B):
+                rec = (sm[b] < 0).nonzero().flatten()
+                if rec.numel():
+                    xr = x0[b, rec][None]
+                    for blk in model.blocks:
+                        xr = blk(xr)
+                    h[b, rec] = model.ln(xr)[0]
+                keep = (sm[b] >= 0).nonzero().flatten()
+                if keep.numel():
+                    h[b, keep] = hc[b, sm[b, keep]]
+            hc = h
+            assert float(cosine(y, h).min()) > 0.999, t
+        enc.check()
+        eager.check()
+
+
 def test_inplace_splice_matches_oracle(cuda):
     """fc_splice_inplace: zero-displacement streams update in place (reused
     rows untouched), shifted streams ping-pong; results equal the oracle
