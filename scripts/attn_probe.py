@@ -75,3 +75,44 @@ for be in (SDPBackend.CUDNN_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBacken
 flops = sum(4 * l * l * H * HD for l in lens)
 res["tflops_at_per_stream"] = flops / res["per_stream_sdpa"] / 1e9
 print(res)
+
+# the padded layout of CachedEncoder's graphed subset path: [B L + 1, 3, H, hdp]
+hdp = 80
+padb = torch.zeros(B * L + 1, 3, H, hdp, device=dev, dtype=torch.bfloat16)
+dense = padb[:-1].unflatten(0, (B, -1))
+qq, kk, vv = (dense[:, :, j].transpose(1, 2) for j in range(3))
+res2 = {}
+res2["padded80_strided_default"] = timeit(lambda: F.scaled_dot_product_attention(qq, kk, vv, scale=HD ** -0.5))
+for be in (SDPBackend.CUDNN_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.FLASH_ATTENTION):
+    try:
+        with sdpa_kernel(be):
+            res2[f"padded80_strided_{be.name}"] = timeit(lambda: F.scaled_dot_product_attention(qq, kk, vv, scale=HD ** -0.5))
+    except Exception as ex:  # noqa: BLE001
+        res2[f"padded80_strided_{be.name}"] = str(ex)[:60]
+qc, kc, vc = (t.contiguous() for t in (qq, kk, vv))
+res2["padded80_contig_default"] = timeit(lambda: F.scaled_dot_product_attention(qc, kc, vc, scale=HD ** -0.5))
+q72 = torch.randn(B, H, L, 72, device=dev, dtype=torch.bfloat16)
+res2["dense72_contig_default"] = timeit(lambda: F.scaled_dot_product_attention(q72, q72, q72))
+print(res2)
+
+# jagged nested tensors through SDPA (which backend torch picks for them)
+offs64 = off.to(torch.int64)
+nj = lambda t: torch.nested.nested_tensor_from_jagged(t, offs64).transpose(1, 2)
+res3 = {}
+try:
+    qn, kn, vn = nj(q), nj(k), nj(v)
+    res3["njt_default"] = timeit(lambda: F.scaled_dot_product_attention(qn, kn, vn))
+    for be in (SDPBackend.CUDNN_ATTENTION, SDPBackend.EFFICIENT_ATTENTION, SDPBackend.FLASH_ATTENTION):
+        try:
+            with sdpa_kernel(be):
+                res3[f"njt_{be.name}"] = timeit(lambda: F.scaled_dot_product_attention(qn, kn, vn))
+        except Exception as ex:  # noqa: BLE001
+            res3[f"njt_{be.name}"] = str(ex)[:60]
+except Exception as ex:  # noqa: BLE001
+    res3["njt"] = str(ex)[:100]
+try:
+    import flashinfer
+    res3["flashinfer"] = flashinfer.__version__
+except Exception as ex:  # noqa: BLE001
+    res3["flashinfer"] = str(ex)[:60]
+print(res3)
