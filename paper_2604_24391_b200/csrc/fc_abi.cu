@@ -65,6 +65,7 @@ struct fc_plan {
   void* fnF = nullptr;
   bool pdl = false;                     // K_C / K_D of the back as programmatic dependents (FC_PDL=1)
   int probe_skip = 0;                  // timing probes only (FC_PROBE_SKIP bitmask): kernels not launched
+  bool probe_back = false;             // timing probes only: FC_PROBE_BACK_PART set at plan creation
   size_t off_flow = 0;
   int kc_ppw = 1;                      // K_C row pairs per warp
   void* fnC = nullptr;
@@ -638,6 +639,7 @@ int fc_plan_create(const fc_geometry* geom, fc_plan** out) {
       // 16 K_D are not launched — results are invalid
       pl->probe_skip = env_int("FC_PROBE_SKIP", 0, 0, 31);
       pl->pdl = env_int("FC_PDL", 0, 0, 1) != 0;
+      pl->probe_back = getenv("FC_PROBE_BACK_PART") != nullptr;
       if (pl->flow_bc) {
         pl->fnF = env_int("FC_BC_DISCARD", 1, 0, 1) ? (void*)k448_bc_flow<6, true> : (void*)k448_bc_flow<6, false>;
         if (rc == FC_OK) rc = set_smem(pl->fnF, pl->smemB);
@@ -742,7 +744,7 @@ int fc_select_back(const fc_plan* pl, const fc_config* cfg, void* state, void* w
   const KParams kp = bind(pl, state, ws, out->energy, slot);
   // timing probe only (scripts/): FC_PROBE_BACK_PART=cols|tail launches one
   // half of the back (no ordering of the shared T2 / sums: results invalid)
-  const char* pp = getenv("FC_PROBE_BACK_PART");
+  const char* pp = pl->probe_back ? getenv("FC_PROBE_BACK_PART") : nullptr;
   const Part part = !pp ? kBack : !strcmp(pp, "cols") ? kCols : !strcmp(pp, "tail") ? kTail : kBack;
   const int lrc = launch_select(pl, *cfg, nullptr, kp, *out, as_stream(stream), nullptr, part);
   if (lrc != FC_OK) return lrc;

@@ -23,7 +23,9 @@ N = 1024
 cache = torch.randn((2, S, N, D), device=dev).to(torch.bfloat16)
 fresh = torch.randn((S, N, D), device=dev).to(torch.bfloat16)
 ages = torch.zeros((2, S, N), dtype=torch.int64, device=dev)
+os.environ["FC_PROBE_BACK_PART"] = "all"   # the plan reads the per-call probe knob (deep variant)
 eng = FreqCacheEngine(S, H, H, P, fmt="rgb")
+del os.environ["FC_PROBE_BACK_PART"]
 spl = SpliceState(cache, ages)
 cfg = CacheConfig(patch_size=P)
 outs = [eng.new_output(), eng.new_output()]
