@@ -153,3 +153,45 @@ def test_fast_path_refuses_misaligned_frames(cuda):
     out = eng.select(buf[:n].view(2, H, H, 3), fc.CacheConfig(patch_size=P))   # aligned: fine
     torch.cuda.synchronize()
     assert (out.host_results()["cold"] == 1).all()
+
+
+@pytest.mark.parametrize("kw,shift", [
+    ({"budget": (0.0, 0.0)}, 1),            # K_reuse = 0: nothing reused
+    ({"budget": (1.0, 1.0)}, 1),            # K_reuse = N: every candidate reused
+    ({"tau_mig": 0.0}, -1),                 # gate never closes on similarity; shift rule off
+    ({"tau_mig": 1.0}, 0),                  # gate closes unless the frames are identical
+    ({"edge_lambda": -5.0}, 1),             # (almost) every token refreshed
+    ({"edge_lambda": 1e12}, 1),             # no token refreshed
+])
+def test_fast_path_config_extremes(cuda, kw, shift):
+    """The 448 x 448 fast path at the configuration extremes (budget 0 / 1,
+    the migration threshold at 0 / 1, refresh thresholds below / above every
+    energy, the config-2 shift rule off / at 0): each stream's decision
+    against the CPU oracle."""
+    import torch
+    import paper_2604_24391_b200 as fc
+    from paper_2604_24391_b200.api import decision_from_device
+    from paper_2604_24391_b200.synth import stream_frames
+    S, T = 4, 3
+    fr = np.stack([stream_frames(4200, s, T, H, H) for s in range(S)], axis=1)
+    fr[2, 3] = fr[1, 3]                      # one identical consecutive pair
+    b = kw.get("budget", (0.08, 0.5))
+    cfg = fc.CacheConfig(patch_size=P, tau_mig=kw.get("tau_mig", 0.12), edge_lambda=kw.get("edge_lambda", 0.25),
+                         budget=fc.BudgetConfig(*b))
+    oc = O.OracleConfig(patch_size=P, tau_mig=cfg.tau_mig, edge_lambda=cfg.edge_lambda, alpha_min=b[0],
+                        alpha_max=b[1], refresh_shift=None if shift < 0 else shift)
+    eng = fc.FreqCacheEngine(S, H, H, P, fmt="rgb")
+    rep = ParityReport()
+    for t in range(T):
+        out = eng.select(torch.from_numpy(np.ascontiguousarray(fr[t])).cuda(), cfg, refresh_shift=shift)
+        if t == 0:
+            continue
+        res = out.host_results()
+        ri, rc, rm = out.reuse_idx.cpu().numpy(), out.recompute_idx.cpu().numpy(), out.refresh_mask.cpu().numpy()
+        en = out.energy.cpu().numpy()
+        for s in range(S):
+            d = decision_from_device(res[s], ri[s], rc[s], rm[s], step=t)
+            compare(d, O.decide(fr[t - 1, s], fr[t, s], oc, step=t), oc, energies=en[s], rep=rep)
+            if b == (0.0, 0.0):
+                assert len(d.reuse_set) == 0
+    assert rep.ok, rep.errors
