@@ -701,7 +701,14 @@ def run_ours(a):
                 "traffic": None, "kernel": names[dom], "peak_kind": peak_kind,
                 "bytes_per_launch": kbytes[dom], "ms_per_launch": kms[dom],
                 "note": "serialised pass, each kernel configured as in the timed step; the splice copier is "
-                        "sized to co-run with the select kernels (1 CTA/SM), see splice_alone_wide"}
+                        "sized to co-run with the select kernels (1 CTA/SM), see splice_alone_wide; splice "
+                        "bytes = the rows it must move (in-place streams skip their reused rows)"}
+    if names[dom] == "splice":
+        # SURVEY 8(d)'s literal per-stream splice figure (the out-of-place
+        # gather's bytes), which the in-place splice undercuts
+        alg = S * (4 * N * D + 20 * N)
+        roofline["bytes_per_launch_8d"] = alg
+        roofline["frac_8d"] = alg / (kms[dom] / 1e3) / 1e9 / hbm
     splice_wide = {"ms": wide_ms, "bytes": wide_bytes, "gbs": wide_bytes / (wide_ms / 1e3) / 1e9,
                    "frac": wide_bytes / (wide_ms / 1e3) / 1e9 / hbm,
                    "config": "FC_SPLICE_BULK_CTAS=2 (2 copier CTAs per SM), same splices, serialised"}
