@@ -3,10 +3,13 @@
 // fp64-derived twiddles, DCT basis), workspace carving and kernel launches.
 //
 // Two kernel sets implement fc_select:
-//   fast    H = W = 448, P = 14 (BASELINE configs 2-5): register-resident
-//           448-point FFTs (fc_fast448.cuh), streams processed in chunks of
-//           kChunk so the two spectrum intermediates (T1, T2: 0.8 MB per
-//           stream each) stay L2-resident between the three FFT kernels;
+//   fast    H = W = 448, P = 14 (BASELINE configs 2-5): warp-owned
+//           448-point FFTs (fc_wfft448.cuh) in K_A / K_B / K_C
+//           (fc_fast448.cuh, fc_fast448w.cuh) over the whole batch as one
+//           chunk (two half-batch chunks on two lanes at <= 128 streams);
+//           the two spectrum intermediates (T1, T2: 0.8 MB per stream each)
+//           make a round trip through HBM (DESIGN §3 lists what was measured
+//           to keep them on chip);
 //   generic any other geometry inside the envelope: shared-memory Stockham
 //           FFTs with runtime radix plans (fc_fft.cuh / fc_kernels.cuh).
 #include <cuda.h>
