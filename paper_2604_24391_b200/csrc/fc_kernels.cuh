@@ -9,10 +9,17 @@
 //                     normalised cross-power, inverse column FFT -> T.
 //   K_C  k_rows_inv   RG rows of T: packed complex-to-real inverse row FFT,
 //                     phase-correlation argmax with the reference tie rule.
+//   K_D1 k_rank       one CTA per stream, beside K_B / K_C: energy mean / std,
+//                     refresh mask, the ascending (E, index) order of every
+//                     token (register + shared-memory bitonic network).
 //   K_D  k_select     one CTA per stream: reductions, gate, displacement,
-//                     alignment, refresh mask, budget, ascending-energy top-K
-//                     (bitonic), recompute order, splice map, outputs.
-//   K_E  k_splice     bf16 (any dtype) hidden-state gather/scatter + ages.
+//                     alignment, budget, the first K_final candidates of
+//                     K_D1's order (one prefix scan), recompute order, splice
+//                     map, outputs, run_sequence counters.
+//   K_E  k_splice*    bf16 (any dtype) hidden-state gather/scatter + ages;
+//                     k_splice_plan + k_splice_ip_bulk: the in-place TMA form.
+// (These are the generic-geometry kernels plus the shared K_D1 / K_D / K_E;
+// the 448 x 448 / P 14 forms of K_A / K_B / K_C are in fc_fast448*.cuh.)
 //
 // Reference semantics cited per kernel; the layout of T / state is private:
 // [B][NCB][H][CB] float2, CB packed columns per block, where packed column 0
