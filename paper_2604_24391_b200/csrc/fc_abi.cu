@@ -263,8 +263,11 @@ void launch_rank(const fc_plan* pl, const fc_config& cfg, const KParams& kp, int
     cudaStreamWaitEvent(pl->aux, pl->ev_a, 0);
     rs = pl->aux;
   }
+  // FC_RANK_NT: threads per stream of K_D1 (default 512 at <= 128 streams)
+  static const int rank_nt = env_int("FC_RANK_NT", 0, 0, 512);
+  const bool wide = rank_nt ? rank_nt >= 512 : nb <= kSmallBatch;
   if (pl->probe_skip & 2) {
-  } else if (nb <= kSmallBatch) {
+  } else if (wide) {
     k_rank<512><<<nb, 512, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
   } else {
     k_rank<FC_SEL_THREADS><<<nb, FC_SEL_THREADS, pl->smemR, rs>>>(kp, cfg.edge_lambda, b0);
