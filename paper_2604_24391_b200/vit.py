@@ -42,6 +42,10 @@ try:  # variable-length attention for the packed subset mode (library kernel)
     from flash_attn import flash_attn_varlen_func as _flash_varlen
 except Exception:  # noqa: BLE001 - optional dependency
     _flash_varlen = None
+try:  # cuDNN ragged attention through flashinfer's wrapper (library kernel)
+    from flashinfer.prefill import cudnn_batch_prefill_with_kv_cache as _cudnn_ragged
+except Exception:  # noqa: BLE001 - optional dependency
+    _cudnn_ragged = None
 
 
 @dataclass(frozen=True)
@@ -90,14 +94,24 @@ class Block(torch.nn.Module):
         x = x + self.attn(y, y, key_padding)
         return x + self.fc2(F.gelu(self.fc1(self.ln2(x)), approximate="tanh"))
 
-    def forward_packed(self, x, offsets, max_len):
+    def forward_packed(self, x, offsets, max_len, ragged=None):
         """Block over variable-length token sets packed as [T, D] (stream b's
         tokens at rows offsets[b] .. offsets[b+1]); attention stays within a
-        stream: flash-attention varlen (library kernel) on [T, heads, hd],
-        or jagged nested tensors through SDPA where flash_attn is absent."""
+        stream: ``ragged(q, k, v)`` (cuDNN ragged attention on contiguous
+        [T, heads, hd] q / k / v) when given, else flash-attention varlen
+        (library kernel) on strided views, else jagged nested tensors through
+        SDPA where flash_attn is absent."""
         y = self.ln1(x)
         d = x.shape[-1]
         hd = d // self.h
+        if ragged is not None:
+            # three projections, so q, k and v are each contiguous (the
+            # ragged kernel takes token-contiguous rows)
+            w, bias = self.qkv.weight.split(d), self.qkv.bias.split(d)
+            q, k, v = (F.linear(y, w[j], bias[j]).view(-1, self.h, hd) for j in range(3))
+            o = ragged(q, k, v)
+            x = x + self.proj(o.reshape(-1, d))
+            return x + self.fc2(F.gelu(self.fc1(self.ln2(x)), approximate="tanh"))
         q, k, v = (t.unflatten(-1, (self.h, hd)) for t in
                    F.linear(y, self.qkv.weight, self.qkv.bias).split(d, dim=-1))
         if _flash_varlen is not None and x.dtype in (torch.float16, torch.bfloat16):
@@ -205,6 +219,14 @@ class CachedEncoder:
         # padding segments inside a graph; other dtypes run eagerly)
         self.sub_graphs = ({} if (graphs and mode == "subset" and _flash_varlen is not None
                                   and dt in (torch.float16, torch.bfloat16)) else None)
+        # graphed subset attention: cuDNN ragged attention (flashinfer's
+        # wrapper) where available, 2.2x faster than flash-attention varlen on
+        # B200 at head dim 72 (scripts/attn_probe2.py); FC_VIT_ATTN=fa2 keeps
+        # flash-attention
+        self.cudnn_attn = (self.sub_graphs is not None and _cudnn_ragged is not None
+                           and os.environ.get("FC_VIT_ATTN", "cudnn") == "cudnn")
+        if self.cudnn_attn:
+            self.attn_ws = torch.empty(256 << 20, dtype=torch.uint8, device=device)
         nb = batch * n
         self.bucket = max(64, min(1024, -(-nb // 16 // 64) * 64))   # ~16 row buckets
         if self.b0_graphs is not None or self.sub_graphs is not None:
@@ -416,8 +438,21 @@ class CachedEncoder:
         x = m.embed(self._embed_input(self.st_frames, flat, dt)) + m.pos.index_select(0, tok)
         # segments: the B streams (empty ones have zero length), then padding
         seg = torch.cat([offsets, torch.full((1,), tp, dtype=offsets.dtype, device=self.device)])
+        ragged = None
+        if self.cudnn_attn:
+            h = m.c.heads
+            hd = m.c.width // h
+            lens = (seg[1:] - seg[:-1]).to(torch.int32).view(-1, 1, 1, 1)
+            rows = (seg * (h * hd)).to(torch.int32).view(-1, 1, 1, 1)     # element offsets of each segment
+            ws, mx = self.attn_ws, max(n, self.bucket)
+
+            def ragged(q, k, v):
+                return _cudnn_ragged(q, k, v, hd ** -0.5, ws, max_token_per_sequence=mx, max_sequence_kv=mx,
+                                     actual_seq_lens_q=lens, actual_seq_lens_kv=lens, causal=False,
+                                     return_lse=False, batch_offsets_q=rows, batch_offsets_o=rows,
+                                     batch_offsets_k=rows, batch_offsets_v=rows, is_cuda_graph_compatible=True)[0]
         for blk in m.blocks:
-            x = blk.forward_packed(x, seg, max(n, self.bucket))
+            x = blk.forward_packed(x, seg, max(n, self.bucket), ragged)
         packed = m.ln(x)
         splice_packed(self.st_src, self.h1[i], self.ages[i], packed, offsets[:B], self.h1[o], self.ages[o],
                       status=self.status)

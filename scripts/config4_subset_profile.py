@@ -34,4 +34,4 @@ with torch.no_grad():
             fn()
             torch.cuda.synchronize()
         print(f"===== {name} ({T - 4} steps)")
-        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=18, max_name_column_width=70))
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=30, max_name_column_width=70))
