@@ -20,8 +20,10 @@ Two cached-step modes (``CachedEncoder.step``):
   states; recomputed tokens run the whole encoder attending among
   themselves, reused tokens take their (displacement-mapped) cached final
   state.  The recomputed tokens of all streams are packed without padding
-  ([sum K_b, D] GEMMs, jagged-nested SDPA per stream), so the encoder work
-  scales with the recompute ratio.
+  ([sum K_b, D] GEMMs; attention within each stream by cuDNN's ragged
+  kernel, else flash-attention varlen, else jagged-nested SDPA), so the
+  encoder work scales with the recompute ratio; the bf16 step replays from a
+  CUDA graph per packed-row bucket.
 
 Both splice through ``fc_splice`` (bf16, bit copies, device-side bounds
 check) with the select's ``src_map``, and both report the cosine similarity
