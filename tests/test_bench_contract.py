@@ -128,3 +128,53 @@ def test_gpu_two_ranks_one_device():
     w = d["weak_scaling"]
     assert w["streams_total"] == 32 and w["streams_per_gpu"] == 16 and w["value"] > 0
     assert abs(w["value"] - 32 / (w["ms_per_step"] / 1e3)) / w["value"] < 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("graph_steps,no_graph", [(1, False), (2, False), (1, True)])
+def test_gpu_bench_pipeline_matches_serial(cuda, graph_steps, no_graph):
+    """The benchmark's own timed path — bench.Pipeline: front of t + 1 beside
+    back of t beside the in-place splice of t - 1 on three streams, replayed
+    from per-ring-phase CUDA graphs (or chunks of graph_steps steps without
+    per-step joins, or eager) — leaves every stream's token cache, ages and
+    last decision bit-identical to plain select-then-splice per step: no
+    race between the branches, slots or ping-pong buffers."""
+    import argparse
+    import torch
+    import bench
+    import paper_2604_24391_b200 as fc
+    S, R, D = 24, 4, 64
+    a = argparse.Namespace(size=448, patch=14, dim=D, no_pipeline=False, no_graph=no_graph,
+                           graph_steps=graph_steps, refresh_shift=1)
+    dev = torch.device("cuda", 0)
+    pl = bench.Pipeline(a, dev, S, 0, 0, R)
+    torch.cuda.synchronize()
+    cache0, ages0 = pl.spl.cache[0].clone(), pl.spl.ages[0].clone()   # no splice has run yet
+    pl.advance(2 * R + 1)
+    t_last = pl.t_next - 1
+    pl.spl.step(pl.outs[t_last & 1].src_map, pl.fresh)          # the pending splice of the last step
+    torch.cuda.synchronize()
+    tok, age = pl.spl.current()
+
+    eng = fc.FreqCacheEngine(S, 448, 448, 14, fmt="rgb", device=dev)
+    N = eng.n_tokens
+    cache = torch.zeros((2, S, N, D), dtype=torch.bfloat16, device=dev)
+    ages = torch.zeros((2, S, N), dtype=torch.int64, device=dev)
+    cache[0], ages[0] = cache0, ages0
+    ref = fc.SpliceState(cache, ages)
+    for t in range(t_last + 1):
+        out = eng.select(pl.frames[t % R], pl.cfg, refresh_shift=1)
+        ref.step(out.src_map, pl.fresh)
+    torch.cuda.synchronize()
+    rtok, rage = ref.current()
+    last = pl.outs[t_last & 1]
+    for name in ("results", "src_map", "reuse_idx", "recompute_idx", "refresh_mask", "energy"):
+        assert torch.equal(getattr(last, name), getattr(out, name)), name
+    assert torch.equal(tok.view(torch.int16), rtok.view(torch.int16))
+    assert torch.equal(age, rage)
+    # the run exercised the splice: recomputed rows replaced, reused rows aged,
+    # and some streams shifted (ping-pong buffers)
+    moved = (tok.view(torch.int16) != cache0.view(torch.int16)).any(-1).float().mean().item()
+    assert moved > 0.2 and int(age.max()) >= 2
+    assert bool(pl.spl.slot.any()) and not bool(pl.spl.slot.all())
+    pl.spl.check()
