@@ -417,6 +417,17 @@ class Pipeline:
         bs = torch.cuda.Stream(dev, priority=int(os.environ.get("FC_BENCH_BACK_PRIO", "0")))
         rs = a.refresh_shift
 
+        # the splice of t - 1 gets 2 more copier CTAs per SM once the back of
+        # t is done (they take only unclaimed rows): +0.7 % at 512 streams,
+        # -1 % at 64, so on above 128 streams per GPU;
+        # FC_BENCH_SPLICE_BOOST=c sets the CTA count (0: off)
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        boost = int(os.environ.get("FC_BENCH_SPLICE_BOOST", str(2 * nsm if S > 128 else 0)))
+        if boost > 0 and not a.no_pipeline:
+            self.per_phase += 1          # the extra copier launch
+        self.boost = boost if not a.no_pipeline else 0
+        boost_on_front = os.environ.get("FC_BENCH_SPLICE_BOOST_ON", "back") == "front"
+
         def phase(t):
             cur = torch.cuda.current_stream(dev)
             side.wait_stream(cur)
@@ -431,13 +442,16 @@ class Pipeline:
                 bs.wait_stream(cur)
                 with torch.cuda.stream(bs):
                     eng.select_back(cfg, outs[t & 1], t & 1, refresh_shift=rs)
-                cur.wait_stream(bs)
             if t > 0:
                 with torch.cuda.stream(side):
-                    spl.step(outs[(t - 1) & 1].src_map, fresh)
+                    spl.step(outs[(t - 1) & 1].src_map, fresh, boostable=boost > 0 and not a.no_pipeline)
                 n_spliced[0] += 1
+                if boost > 0 and not a.no_pipeline:
+                    with torch.cuda.stream(fs if boost_on_front else bs):
+                        spl.boost(boost)
                 cur.wait_stream(side)
             if not a.no_pipeline:
+                cur.wait_stream(bs)
                 cur.wait_stream(fs)
 
         ev = {k: [torch.cuda.Event(), torch.cuda.Event()] for k in ("front", "back", "splice")}
@@ -905,6 +919,7 @@ def run_ours(a):
                                     ": select + splice, adaptive budget, refresh on shift>1"),
                        "graph": not a.no_graph, "pipeline": not a.no_pipeline,
                        "graph_steps": pl.G if not a.no_graph else 0,
+                       "splice_boost_ctas": pl.boost,
                        "streams_per_gpu": S, "streams_total": total_streams, "size": H, "channels": 3, "patch": P, "tokens": N,
                        "hidden": D, "hidden_dtype": "bf16", "frame_ring_steps": R,
                        "l2": f"inputs > L2 ({S * H * H * 12 / 1e9:.2f} GB of frames per step, "

@@ -254,6 +254,27 @@ int  fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes,
                        int32_t fresh_rows, void* scratch, int32_t* status,
                        void* cuda_stream);
 
+/* fc_splice_inplace in two halves, for spreading one splice over two
+ * streams: _plan (the per-stream in-place / ping-pong decision, the rows to
+ * move and the copier's work counter) and _copy (copier CTAs that claim those
+ * rows).  _copy with ctas = 0 is the default copier; a further _copy with
+ * ctas > 0 on another stream, ordered after the plan (an event recorded right
+ * after _plan), adds CTAs that take only the rows no copier has claimed yet
+ * — e.g. launched behind the select kernels, it finishes the tail of a
+ * splice that ran beside them.  All copies of one splice must complete before
+ * the next splice's _plan.  fc_splice_inplace = _plan + _copy(0). */
+int  fc_splice_inplace_plan(int32_t batch, int32_t n_tokens, int64_t row_bytes,
+                            const int32_t* src_map, void* cache0, void* cache1,
+                            int64_t* ages0, int64_t* ages1, const uint8_t* slot_in,
+                            uint8_t* slot_out, const void* fresh, int32_t fresh_layout,
+                            int32_t fresh_rows, void* scratch, void* cuda_stream);
+int  fc_splice_inplace_copy(int32_t batch, int32_t n_tokens, int64_t row_bytes,
+                            const int32_t* src_map, void* cache0, void* cache1,
+                            int64_t* ages0, int64_t* ages1, const uint8_t* slot_in,
+                            const uint8_t* slot_out, const void* fresh, int32_t fresh_layout,
+                            int32_t fresh_rows, void* scratch, int32_t* status,
+                            int32_t ctas, void* cuda_stream);
+
 /* Build src_map for one stream from an ordered reuse list (fusion.py:481-504).
  * flag (device int32, may be NULL) receives FC_EBOUNDS on an out-of-bounds
  * source. */

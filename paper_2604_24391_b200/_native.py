@@ -45,7 +45,7 @@ EXPORTS = (
     "fc_state_reset", "fc_select", "fc_select_front", "fc_select_back", "fc_select_profile", "fc_patch_energy", "fc_splice",
     "fc_splice_map", "fc_stage_workspace_bytes", "fc_amp_cosine", "fc_spectral_sums",
     "fc_refresh_mask", "fc_topk_ascending", "fc_render_masks", "fc_splice_packed",
-    "fc_splice_inplace", "fc_splice_inplace_scratch_bytes", "fc_compare_cosines", "fc_row_cosines",
+    "fc_splice_inplace", "fc_splice_inplace_plan", "fc_splice_inplace_copy", "fc_splice_inplace_scratch_bytes", "fc_compare_cosines", "fc_row_cosines",
     "fc_graph_capture_begin", "fc_graph_capture_end", "fc_graph_launch", "fc_graph_destroy",
     "fc_dft2_workspace_bytes", "fc_dft2", "fc_phase_correlation_workspace_bytes", "fc_phase_correlation_spectra",
     "fc_block_dct", "fc_amplitude_phase", "fc_gather_patches",
@@ -124,6 +124,9 @@ def load(path=None):
         "fc_render_masks": (C.c_int, [i32, i32, vp, vp, vp, vp, vp]),
         "fc_splice_packed": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "fc_splice_inplace": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]),
+        "fc_splice_inplace_plan": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]),
+        "fc_splice_inplace_copy": (C.c_int, [i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, i32,
+                                             vp]),
         "fc_splice_inplace_scratch_bytes": (i64, [i32, i32]),
         "fc_amp_cosine": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
         "fc_spectral_sums": (C.c_int, [vp, i64, i32, vp, vp, vp, vp]),

@@ -885,10 +885,13 @@ int64_t fc_splice_inplace_scratch_bytes(int32_t batch, int32_t n_tokens) {
   return (int64_t)batch * n_tokens * 4 + (int64_t)batch * 4 + 256;
 }
 
-int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, void* cache0,
-                      void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in, uint8_t* slot_out,
-                      const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* scratch, int32_t* status,
-                      void* stream) {
+}  // extern "C"
+
+namespace {
+
+int splice_ip_check(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, void* cache0,
+                    void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in, uint8_t* slot_out,
+                    const void* fresh, int32_t fresh_layout, int32_t& fresh_rows, void* scratch) {
   if (batch < 1 || n_tokens < 1 || row_bytes < 16 || row_bytes % 16 || !src_map || !cache0 || !cache1 || !ages0 ||
       !ages1 || !slot_in || !slot_out || !fresh || !scratch)
     return FC_EINVAL;
@@ -899,10 +902,69 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
   if ((int64_t)batch * n_tokens > INT32_MAX || row_bytes > INT32_MAX) return FC_EINVAL;
   if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
   if (fresh_rows < 1) return FC_EINVAL;
-  const cudaStream_t st = as_stream(stream);
+  return FC_OK;
+}
+
+// The copy half of the in-place splice: copier CTAs claiming the planned
+// rows from the plan's work counter.  ctas > 0 sets the copier's CTA count
+// (an extra launch then only takes the rows no earlier copier has claimed).
+int splice_ip_copy(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, void* cache0,
+                   void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in, const uint8_t* slot_out,
+                   const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* scratch, int32_t* status,
+                   int ctas, cudaStream_t st);
+
+}  // namespace
+
+extern "C" {
+
+int fc_splice_inplace_plan(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map,
+                           void* cache0, void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in,
+                           uint8_t* slot_out, const void* fresh, int32_t fresh_layout, int32_t fresh_rows,
+                           void* scratch, void* stream) {
+  const int rc = splice_ip_check(batch, n_tokens, row_bytes, src_map, cache0, cache1, ages0, ages1, slot_in, slot_out,
+                                 fresh, fresh_layout, fresh_rows, scratch);
+  if (rc != FC_OK) return rc;
   int32_t* rows = reinterpret_cast<int32_t*>(scratch);
   int32_t* counts = rows + (size_t)batch * n_tokens;
-  k_splice_plan<<<batch, 256, 0, st>>>(n_tokens, src_map, slot_in, slot_out, ages0, ages1, rows, counts);
+  k_splice_plan<<<batch, 256, 0, as_stream(stream)>>>(n_tokens, src_map, slot_in, slot_out, ages0, ages1, rows,
+                                                       counts);
+  return launch_check();
+}
+
+int fc_splice_inplace_copy(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map,
+                           void* cache0, void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in,
+                           const uint8_t* slot_out, const void* fresh, int32_t fresh_layout, int32_t fresh_rows,
+                           void* scratch, int32_t* status, int32_t ctas, void* stream) {
+  if (ctas < 0) return FC_EINVAL;
+  const int rc = splice_ip_check(batch, n_tokens, row_bytes, src_map, cache0, cache1, ages0, ages1, slot_in,
+                                 const_cast<uint8_t*>(slot_out), fresh, fresh_layout, fresh_rows, scratch);
+  if (rc != FC_OK) return rc;
+  return splice_ip_copy(batch, n_tokens, row_bytes, src_map, cache0, cache1, ages0, ages1, slot_in, slot_out, fresh,
+                        fresh_layout, fresh_rows, scratch, status, ctas, as_stream(stream));
+}
+
+int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, void* cache0,
+                      void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in, uint8_t* slot_out,
+                      const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* scratch, int32_t* status,
+                      void* stream) {
+  const int rc = fc_splice_inplace_plan(batch, n_tokens, row_bytes, src_map, cache0, cache1, ages0, ages1, slot_in,
+                                        slot_out, fresh, fresh_layout, fresh_rows, scratch, stream);
+  if (rc != FC_OK) return rc;
+  if (fresh_layout == FC_FRESH_DENSE) fresh_rows = n_tokens;
+  return splice_ip_copy(batch, n_tokens, row_bytes, src_map, cache0, cache1, ages0, ages1, slot_in, slot_out, fresh,
+                        fresh_layout, fresh_rows, scratch, status, 0, as_stream(stream));
+}
+
+}  // extern "C"
+
+namespace {
+
+int splice_ip_copy(int32_t batch, int32_t n_tokens, int64_t row_bytes, const int32_t* src_map, void* cache0,
+                   void* cache1, int64_t* ages0, int64_t* ages1, const uint8_t* slot_in, const uint8_t* slot_out,
+                   const void* fresh, int32_t fresh_layout, int32_t fresh_rows, void* scratch, int32_t* status,
+                   int ctas, cudaStream_t st) {
+  int32_t* rows = reinterpret_cast<int32_t*>(scratch);
+  int32_t* counts = rows + (size_t)batch * n_tokens;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -918,7 +980,7 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
     const int per_sm = env_int("FC_SPLICE_BULK_CTAS", 1, 1, 32);
     // FC_SPLICE_BULK_GRID: absolute copier CTA count (overrides per-SM sizing)
     const int grid_abs = env_int("FC_SPLICE_BULK_GRID", 0, 0, 1 << 16);
-    const int grid = grid_abs > 0 ? grid_abs : sms * per_sm;
+    const int grid = ctas > 0 ? ctas : grid_abs > 0 ? grid_abs : sms * per_sm;
     auto fn = pick_bulk(NL, SL);  // the (NL, SL) instance bulk_smem was sized for
     if (bulk_smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem);
     fn<<<grid, 32, bulk_smem, st>>>(
@@ -927,6 +989,9 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
         fresh_layout == FC_FRESH_COMPACT, fresh_rows, status);
     return launch_check();
   }
+  // the non-TMA copier partitions the rows statically: an extra launch has
+  // nothing left to claim
+  if (ctas > 0) return FC_OK;
   const int total = batch * n_tokens;
   constexpr int UNR = 2;
   int blocks = ((total + UNR - 1) / UNR + (FC_THREADS / 32) - 1) / (FC_THREADS / 32);
@@ -937,6 +1002,10 @@ int fc_splice_inplace(int32_t batch, int32_t n_tokens, int64_t row_bytes, const 
       fresh_layout == FC_FRESH_COMPACT, fresh_rows, status);
   return launch_check();
 }
+
+}  // namespace
+
+extern "C" {
 
 int fc_compare_cosines(const fc_geometry* geom, const void* prev, const void* curr, double* visual_cos,
                        double* naive_cos, void* stream) {

@@ -382,12 +382,17 @@ class SpliceState:
         nb = nat.lib().fc_splice_inplace_scratch_bytes(int(B), int(cache.shape[2]))
         self.scratch = torch.empty(nb, dtype=torch.uint8, device=cache.device)
         self.status = _status_word(cache.device)
+        self.plan_done = None      # event after the last boostable splice's plan
+        self._boost_args = None
 
     @property
     def slot(self):
         return self.slots[self.k]
 
-    def step(self, src_map, fresh, compact=False):
+    def step(self, src_map, fresh, compact=False, boostable=False):
+        """One splice on the current stream.  ``boostable``: issued as plan +
+        copy with an event between them, so :meth:`boost` can later add
+        copier CTAs to this splice from another stream."""
         lib = nat.lib()
         dev = self.cache.device
         if (src_map.dtype != torch.int32 or tuple(src_map.shape) != tuple(self.cache.shape[1:3])
@@ -403,14 +408,36 @@ class SpliceState:
         if not compact and fresh.shape[1] != N:
             raise ValueError("dense fresh must be [B, N, D]")
         sin, sout = self.slots[self.k], self.slots[1 - self.k]
-        rc = lib.fc_splice_inplace(int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(self.cache[0]),
-                                   _ptr(self.cache[1]), _ptr(self.ages[0]), _ptr(self.ages[1]), _ptr(sin),
-                                   _ptr(sout), _ptr(fresh),
-                                   nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE, int(fresh.shape[1]),
-                                   _ptr(self.scratch), _ptr(self.status), _stream(self.cache.device))
-        nat.check(rc, "fc_splice_inplace")
+        layout = nat.FC_FRESH_COMPACT if compact else nat.FC_FRESH_DENSE
+        args = (int(B), int(N), int(row_bytes), _ptr(src_map), _ptr(self.cache[0]), _ptr(self.cache[1]),
+                _ptr(self.ages[0]), _ptr(self.ages[1]), _ptr(sin), _ptr(sout), _ptr(fresh), layout,
+                int(fresh.shape[1]), _ptr(self.scratch))
+        st = _stream(self.cache.device)
+        if boostable:
+            nat.check(lib.fc_splice_inplace_plan(*args, st), "fc_splice_inplace_plan")
+            if self.plan_done is None:
+                self.plan_done = torch.cuda.Event()
+            self.plan_done.record(torch.cuda.current_stream(dev))
+            nat.check(lib.fc_splice_inplace_copy(*args, _ptr(self.status), 0, st), "fc_splice_inplace_copy")
+            self._boost_args = args
+        else:
+            rc = lib.fc_splice_inplace(*args, _ptr(self.status), st)
+            nat.check(rc, "fc_splice_inplace")
+            self._boost_args = None
         self.k = 1 - self.k
         return self.slot
+
+    def boost(self, ctas):
+        """Add ``ctas`` copier CTAs, on the current stream, to the last
+        ``boostable`` splice: they wait for its plan and take only rows no
+        copier has claimed yet (fc_splice_inplace_copy).  Must complete before
+        the next step's splice (join the streams)."""
+        if self._boost_args is None:
+            raise RuntimeError("boost() needs a preceding step(..., boostable=True)")
+        dev = self.cache.device
+        torch.cuda.current_stream(dev).wait_event(self.plan_done)
+        nat.check(nat.lib().fc_splice_inplace_copy(*self._boost_args, _ptr(self.status), int(ctas),
+                                                   _stream(dev)), "fc_splice_inplace_copy")
 
     def check(self):
         """Raise AssertionError if any step so far met an out-of-bounds

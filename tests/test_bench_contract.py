@@ -131,14 +131,16 @@ def test_gpu_two_ranks_one_device():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("graph_steps,no_graph", [(1, False), (2, False), (1, True)])
-def test_gpu_bench_pipeline_matches_serial(cuda, graph_steps, no_graph):
+@pytest.mark.parametrize("graph_steps,no_graph,boost", [(1, False, "0"), (2, False, "0"), (1, True, "0"),
+                                                        (1, False, "296"), (1, True, "148")])
+def test_gpu_bench_pipeline_matches_serial(cuda, monkeypatch, graph_steps, no_graph, boost):
     """The benchmark's own timed path — bench.Pipeline: front of t + 1 beside
     back of t beside the in-place splice of t - 1 on three streams, replayed
     from per-ring-phase CUDA graphs (or chunks of graph_steps steps without
     per-step joins, or eager) — leaves every stream's token cache, ages and
     last decision bit-identical to plain select-then-splice per step: no
-    race between the branches, slots or ping-pong buffers."""
+    race between the branches, slots or ping-pong buffers — also with extra
+    copier CTAs joining each splice from the back's stream (the boost)."""
     import argparse
     import torch
     import bench
@@ -147,6 +149,7 @@ def test_gpu_bench_pipeline_matches_serial(cuda, graph_steps, no_graph):
     a = argparse.Namespace(size=448, patch=14, dim=D, no_pipeline=False, no_graph=no_graph,
                            graph_steps=graph_steps, refresh_shift=1)
     dev = torch.device("cuda", 0)
+    monkeypatch.setenv("FC_BENCH_SPLICE_BOOST", boost)
     pl = bench.Pipeline(a, dev, S, 0, 0, R)
     torch.cuda.synchronize()
     cache0, ages0 = pl.spl.cache[0].clone(), pl.spl.ages[0].clone()   # no splice has run yet
