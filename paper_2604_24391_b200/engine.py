@@ -431,7 +431,8 @@ class SpliceState:
         """Add ``ctas`` copier CTAs, on the current stream, to the last
         ``boostable`` splice: they wait for its plan and take only rows no
         copier has claimed yet (fc_splice_inplace_copy).  Must complete before
-        the next step's splice (join the streams)."""
+        the next step's splice (join the streams); that step's ``src_map`` and
+        ``fresh`` tensors must stay alive until then (the launch reads them)."""
         if self._boost_args is None:
             raise RuntimeError("boost() needs a preceding step(..., boostable=True)")
         dev = self.cache.device
