@@ -688,3 +688,18 @@ def test_gather_patches_matches_torch_patchify(cuda):
     got = gather_patches(frames, 14, idx)
     ref = model.patches(frames.to(torch.bfloat16)).reshape(-1, 3 * 14 * 14).index_select(0, idx)
     assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
+
+
+def test_c_abi_from_plain_c(cuda):
+    """examples/select_c.c: the C ABI driven from C99 through cudart (no
+    Python, no torch) — two shifted 448 x 448 RGB streams; the displacement
+    and every reused token's source must come out as the shift dictates."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run(["make", "-s", "-C", str(root / "examples"), "select_c"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(root / "examples" / "select_c")], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("OK")
+    assert "di_patches 1 " in r.stdout and "di_patches 2 " in r.stdout

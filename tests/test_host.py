@@ -238,3 +238,27 @@ def test_new_entry_points_refuse_bad_arguments_without_device(lib):
     assert lib.fc_graph_launch(None, None) == E
     assert lib.fc_graph_capture_end(None, None) == E
     assert lib.fc_plan_launches(None) == -1
+
+
+def test_header_is_plain_c_and_the_c_example_links(lib, tmp_path):
+    """The boundary is a C ABI: the header compiles as strict C99 on its own
+    (no C++ or torch types), and examples/select_c.c — the ABI driven from
+    plain C through cudart — builds and links against the in-tree library
+    (it runs in the GPU suite)."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    src = tmp_path / "h.c"
+    src.write_text('#include "freqcache_b200.h"\nint main(void) { fc_geometry g = {1, 16, 16, 8, FC_FMT_GRAY_F32};'
+                   ' return g.batch - 1 + (int)sizeof(fc_stream_result) * 0; }\n')
+    r = subprocess.run([gcc, "-std=c99", "-pedantic", "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
+                        f"-I{ROOT / 'include'}", str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    cuda_inc = Path("/usr/local/cuda/include/cuda_runtime_api.h")
+    if not cuda_inc.exists() or shutil.which("make") is None:
+        pytest.skip("no CUDA headers / make")
+    r = subprocess.run(["make", "-s", "-C", str(ROOT / "examples"), "select_c"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert (ROOT / "examples" / "select_c").exists()
