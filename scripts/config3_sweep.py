@@ -6,6 +6,11 @@ time of select + in-place splice per step (CUDA events, 20 steps after
 warm-up, frames from a resident 4-step ring, serial launch order), frames/s,
 and the splice's bytes moved and GB/s.  Prints one JSON object per r and a
 summary list; `--out` writes the list.
+
+Launch order is serial, so the splice runs alone: its copier is sized as
+for a standalone splice (FC_SPLICE_BULK_CTAS=2, two CTAs per SM) unless the
+environment says otherwise — the 1-CTA/SM default is sized to co-run with
+the select kernels in the pipelined step.
 """
 
 import argparse
@@ -17,7 +22,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
-import paper_2604_24391_b200 as fc
+os.environ.setdefault("FC_SPLICE_BULK_CTAS", "2")
+import paper_2604_24391_b200 as fc  # noqa: E402
 from paper_2604_24391_b200.synth import torch_stream_frames
 
 
