@@ -6,7 +6,8 @@ hidden states).  Time only: it approximates the paper's "cuFFT + SIMT"
 implementation and is NOT the product (no tie rules, no failure semantics).
 
 Prints one JSON object: ms per step of the torch composition and of this
-repo's path (fc_select + in-place splice, serial launch order), same inputs.
+repo's path (fc_select + in-place splice, serial launch order, the splice
+copier at its standalone sizing, FC_SPLICE_BULK_CTAS=2), same inputs.
 """
 
 import json
@@ -18,8 +19,9 @@ import math
 
 import torch
 
-import paper_2604_24391_b200 as fc
-from paper_2604_24391_b200.synth import torch_stream_frames
+os.environ.setdefault("FC_SPLICE_BULK_CTAS", "2")   # serial order: the splice runs alone
+import paper_2604_24391_b200 as fc  # noqa: E402
+from paper_2604_24391_b200.synth import torch_stream_frames  # noqa: E402
 
 S, H, P, D, R = int(os.environ.get("S", 512)), 448, 14, 1152, 4
 G = H // P
