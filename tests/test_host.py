@@ -238,6 +238,13 @@ def test_new_entry_points_refuse_bad_arguments_without_device(lib):
     assert lib.fc_graph_launch(None, None) == E
     assert lib.fc_graph_capture_end(None, None) == E
     assert lib.fc_plan_launches(None) == -1
+    # the split in-place splice: same argument rules as fc_splice_inplace
+    args = (2, 16, 64, p, p, p, p, p, p, p, p, _native.FC_FRESH_DENSE, 16, p)
+    assert lib.fc_splice_inplace_plan(0, *args[1:], None) == E                  # batch < 1
+    assert lib.fc_splice_inplace_plan(2, 16, 60, *args[3:], None) == E          # row bytes not a multiple of 16
+    assert lib.fc_splice_inplace_plan(*args[:3], None, *args[4:], None) == E    # no src_map
+    assert lib.fc_splice_inplace_copy(*args, p, -1, None) == E                   # negative CTA count
+    assert lib.fc_splice_inplace_copy(*args[:11], 7, *args[12:], p, 0, None) == E   # bad fresh layout
 
 
 def test_header_is_plain_c_and_the_c_example_links(lib, tmp_path):
