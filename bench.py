@@ -19,7 +19,16 @@ splice of step t - 1) is one CUDA-graph launch.
 
 ``--gpus N`` without torchrun re-launches itself under
 ``torch.distributed.run`` with N ranks (one per GPU, NCCL).  Prints ONE JSON
-line on rank 0.
+line on rank 0; at N > 1 it carries a weak-scaling leg (512 streams per
+rank) beside the strong headline.
+
+Environment (defaults are the measured best): FC_BENCH_SPLICE_BOOST
+(extra copier CTAs joining each splice behind the back branch; 2 per SM above
+128 streams per GPU, else 0), FC_BENCH_SPLICE_BOOST_ON=front, the stream
+priorities FC_BENCH_{SIDE,FRONT,BACK}_PRIO, the library's FC_* kernel knobs;
+FC_BENCH_DEVICE / FC_DIST_BACKEND=gloo run several ranks on one GPU (a
+plumbing check, not a scaling number); FC_BENCH_PLUMBING=1 runs the
+multi-rank reporting path without kernels (CPU tests).
 """
 
 from __future__ import annotations
