@@ -131,9 +131,10 @@ def test_gpu_two_ranks_one_device():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("graph_steps,no_graph,boost", [(1, False, "0"), (2, False, "0"), (1, True, "0"),
-                                                        (1, False, "296"), (1, True, "148")])
-def test_gpu_bench_pipeline_matches_serial(cuda, monkeypatch, graph_steps, no_graph, boost):
+@pytest.mark.parametrize("graph_steps,no_graph,boost,no_pipeline", [
+    (1, False, "0", False), (2, False, "0", False), (1, True, "0", False), (1, False, "296", False),
+    (1, True, "148", False), (1, False, "0", True)])
+def test_gpu_bench_pipeline_matches_serial(cuda, monkeypatch, graph_steps, no_graph, boost, no_pipeline):
     """The benchmark's own timed path — bench.Pipeline: front of t + 1 beside
     back of t beside the in-place splice of t - 1 on three streams, replayed
     from per-ring-phase CUDA graphs (or chunks of graph_steps steps without
@@ -146,7 +147,7 @@ def test_gpu_bench_pipeline_matches_serial(cuda, monkeypatch, graph_steps, no_gr
     import bench
     import paper_2604_24391_b200 as fc
     S, R, D = 24, 4, 64
-    a = argparse.Namespace(size=448, patch=14, dim=D, no_pipeline=False, no_graph=no_graph,
+    a = argparse.Namespace(size=448, patch=14, dim=D, no_pipeline=no_pipeline, no_graph=no_graph,
                            graph_steps=graph_steps, refresh_shift=1)
     dev = torch.device("cuda", 0)
     monkeypatch.setenv("FC_BENCH_SPLICE_BOOST", boost)
